@@ -1,0 +1,752 @@
+// partime_capi.cu: host side of libpartime_b200.so (C ABI in include/partime_b200.h).
+//
+// The handle owns, for every stage local to this process (all on one device):
+//   - padded fp32 weights [n_out, ld_in] and biases, updated in place by the kernel;
+//   - a comm block (stage-input slots x2, stage-output-gradient slots x2 and four
+//     counters). It is cudaMalloc'd on its own so it can be exported over CUDA IPC
+//     to the neighbouring process (one process per GPU; NVLink peer stores);
+//   - three activation-cache slots, g_in partial buffers and step counters.
+// All of it is zeroed at create: warm-up ticks read zero slots.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <string>
+#include <vector>
+
+#include "partime_b200.h"
+#include "pt_kernels.cuh"
+
+using pt::u64;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                            \
+  do {                                                                            \
+    cudaError_t e_ = (expr);                                                      \
+    if (e_ != cudaSuccess)                                                        \
+      return fail(PT_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+#define PT_TRY(expr)          \
+  do {                        \
+    int r_ = (expr);          \
+    if (r_ != PT_OK) return r_; \
+  } while (0)
+
+constexpr int32_t PT_IPC_MAGIC = 0x50544231;  // "PTB1"
+
+// Padded row stride: a power of two in [128, 1024], else a multiple of 2048. Each
+// 128-float segment then maps to one warp, and every column has a fixed owner thread.
+int pad_dim(int n) {
+  if (n <= 128) return 128;
+  if (n <= 1024) {
+    int p = 128;
+    while (p < n) p <<= 1;
+    return p;
+  }
+  return (n + 2047) / 2048 * 2048;
+}
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+// Comm block of one stage (lives on that stage's GPU). The layout is a pure function
+// of (M, ld0, ldk), so every process can address a neighbour's block from the config.
+struct CommLayout {
+  static constexpr size_t IN_READY = 0, G_READY = 128, ACT_CREDIT = 256, G_CREDIT = 384, DATA = 512;
+  size_t inslot_bytes = 0, gslot_bytes = 0, total = 0;
+  CommLayout() = default;
+  CommLayout(int M, int ld0, int ldk) {
+    inslot_bytes = align_up(size_t(M) * ld0 * 4, 256);
+    gslot_bytes = align_up(size_t(M) * ldk * 4, 256);
+    total = DATA + 2 * inslot_bytes + 2 * gslot_bytes;
+  }
+  size_t inslot(int p) const { return DATA + size_t(p) * inslot_bytes; }
+  size_t gslot(int p) const { return DATA + 2 * inslot_bytes + size_t(p) * gslot_bytes; }
+};
+
+struct IpcBlob {
+  int32_t magic, abi, stage, G, M, ld0, ldk, pad_;
+  int64_t comm_bytes;
+  cudaIpcMemHandle_t handle;
+};
+
+struct LayerHost {
+  int n_in = 0, n_out = 0, ld_in = 0, ld_out = 0, act = 0;
+  float* W = nullptr;
+  float* b = nullptr;
+  float* part[2] = {nullptr, nullptr};
+  int rows_per_chunk = 0;
+  int cache_in = 0, cache_out = 0;
+};
+
+struct StageHost {
+  int h = 0;                    // 1-based global stage index
+  int first_global = 0, k = 0;  // global index of first layer, layer count
+  int first_local = 0;          // index into the handle's layer array
+  int ld0 = 0, ldk = 0;
+  char* comm = nullptr;  // own comm block
+  float* cache = nullptr;
+  size_t cache_floats = 0;
+  u64* cnt = nullptr;
+  char* up = nullptr;    // upstream stage's comm block (local or IPC-mapped), h > 1
+  char* down = nullptr;  // downstream stage's comm block, h < D
+  int G_up = 0, G_down = 0;
+};
+
+}  // namespace
+
+struct pt_pipeline {
+  int L = 0, D = 0, M = 1, loss = 0, opt = 0, learn = 1, act_delay = 1;
+  float lr = 0.f;
+  std::vector<int> dims, act, sfl;
+  int local_first = 0, local_count = 0;  // 0-based stage index range owned here
+  int G = 0, device = 0;
+  unsigned long long timeout_ns = 0;
+  bool fast = true;
+  std::vector<LayerHost> layers;  // local layers, global order
+  int layer_base = 0;             // global index of layers[0]
+  std::vector<StageHost> stages;
+  pt::LayerDev* d_layers = nullptr;
+  pt::StageDev* d_stages = nullptr;
+  u64* d_tick_end = nullptr;
+  int* d_status = nullptr;
+  long long* d_first_bad = nullptr;
+  float* xs_pad = nullptr;
+  size_t xs_cap = 0;  // ticks
+  float* ys_stage = nullptr;
+  size_t ys_cap = 0;
+  float* outs_stage = nullptr;
+  size_t outs_cap = 0;
+  float* loss_part = nullptr;
+  size_t lp_cap = 0;
+  float* losses_stage = nullptr;
+  size_t ls_cap = 0;
+  uint8_t* valid_stage = nullptr;
+  size_t vs_cap = 0;
+  float* yhist = nullptr;
+  int yh = 1;
+  cudaStream_t own_stream = nullptr, stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  bool timed = false;
+  long long t_next = 0;
+  bool broken = false;
+  std::atomic<int> busy{0};
+  std::vector<void*> ipc_opened;
+  std::vector<void*> allocs;
+
+  bool has_first() const { return local_first == 0; }
+  bool has_last() const { return local_first + local_count == D; }
+  int F() const { return dims[L]; }
+  int stage_ld0(int s0) const { return pad_dim(dims[sfl[s0]]); }      // s0: 0-based stage
+  int stage_ldk(int s0) const { return pad_dim(dims[sfl[s0 + 1]]); }
+  CommLayout layout_of(int s0) const { return CommLayout(M, stage_ld0(s0), stage_ldk(s0)); }
+};
+
+namespace {
+
+struct BusyGuard {
+  pt_pipeline* p;
+  bool ok;
+  explicit BusyGuard(pt_pipeline* p_) : p(p_) {
+    int z = 0;
+    ok = p->busy.compare_exchange_strong(z, 1);
+  }
+  ~BusyGuard() {
+    if (ok) p->busy.store(0);
+  }
+};
+
+int dev_alloc(pt_pipeline* p, void** ptr, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  CUDA_TRY(cudaMalloc(ptr, bytes));
+  CUDA_TRY(cudaMemset(*ptr, 0, bytes));
+  p->allocs.push_back(*ptr);
+  return PT_OK;
+}
+
+void dev_free(pt_pipeline* p, void* ptr) {
+  if (!ptr) return;
+  for (auto& a : p->allocs)
+    if (a == ptr) a = nullptr;
+  cudaFree(ptr);
+}
+
+// grow a staging buffer (contents not preserved; zeroed so padding stays 0)
+template <typename T>
+int ensure(pt_pipeline* p, T** buf, size_t* cap, size_t need, size_t elems_per) {
+  if (*cap >= need && *buf) return PT_OK;
+  CUDA_TRY(cudaStreamSynchronize(p->stream));
+  dev_free(p, *buf);
+  *buf = nullptr;
+  size_t n = std::max<size_t>(need, 64);
+  PT_TRY(dev_alloc(p, reinterpret_cast<void**>(buf), n * elems_per * sizeof(T)));
+  *cap = n;
+  return PT_OK;
+}
+
+int upload_desc(pt_pipeline* p) {
+  std::vector<pt::LayerDev> ld(p->layers.size());
+  for (size_t i = 0; i < p->layers.size(); ++i) {
+    const LayerHost& h = p->layers[i];
+    pt::LayerDev& d = ld[i];
+    d.W = h.W;
+    d.b = h.b;
+    d.part[0] = h.part[0];
+    d.part[1] = h.part[1];
+    d.n_in = h.n_in;
+    d.n_out = h.n_out;
+    d.ld_in = h.ld_in;
+    d.ld_out = h.ld_out;
+    d.act = h.act;
+    d.rows_per_chunk = h.rows_per_chunk;
+    d.cache_in = h.cache_in;
+    d.cache_out = h.cache_out;
+  }
+  std::vector<pt::StageDev> sd(p->stages.size());
+  for (size_t s = 0; s < p->stages.size(); ++s) {
+    const StageHost& h = p->stages[s];
+    const int s0 = h.h - 1;
+    pt::StageDev& d = sd[s];
+    memset(&d, 0, sizeof(d));
+    d.h = h.h;
+    d.first = h.first_local;
+    d.k = h.k;
+    d.G_up = h.G_up;
+    d.G_down = h.G_down;
+    d.ld0 = h.ld0;
+    d.ldk = h.ldk;
+    for (int j = 0; j < 3; ++j) d.cache[j] = h.cache + size_t(j) * h.cache_floats;
+    const CommLayout own = p->layout_of(s0);
+    for (int j = 0; j < 2; ++j) {
+      d.inslot[j] = reinterpret_cast<float*>(h.comm + own.inslot(j));
+      d.gslot[j] = reinterpret_cast<float*>(h.comm + own.gslot(j));
+    }
+    d.in_ready = reinterpret_cast<u64*>(h.comm + CommLayout::IN_READY);
+    d.g_ready = reinterpret_cast<u64*>(h.comm + CommLayout::G_READY);
+    d.act_credit = reinterpret_cast<u64*>(h.comm + CommLayout::ACT_CREDIT);
+    d.g_credit = reinterpret_cast<u64*>(h.comm + CommLayout::G_CREDIT);
+    if (h.down) {
+      const CommLayout dn = p->layout_of(s0 + 1);
+      for (int j = 0; j < 2; ++j) d.peer_inslot[j] = reinterpret_cast<float*>(h.down + dn.inslot(j));
+      d.peer_in_ready = reinterpret_cast<u64*>(h.down + CommLayout::IN_READY);
+      d.peer_g_credit = reinterpret_cast<u64*>(h.down + CommLayout::G_CREDIT);
+    }
+    if (h.up) {
+      const CommLayout upl = p->layout_of(s0 - 1);
+      for (int j = 0; j < 2; ++j) d.peer_gslot[j] = reinterpret_cast<float*>(h.up + upl.gslot(j));
+      d.peer_g_ready = reinterpret_cast<u64*>(h.up + CommLayout::G_READY);
+      d.peer_act_credit = reinterpret_cast<u64*>(h.up + CommLayout::ACT_CREDIT);
+    }
+    d.cnt = h.cnt;
+  }
+  CUDA_TRY(cudaMemcpy(p->d_layers, ld.data(), ld.size() * sizeof(pt::LayerDev), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(p->d_stages, sd.data(), sd.size() * sizeof(pt::StageDev), cudaMemcpyHostToDevice));
+  return PT_OK;
+}
+
+int validate(const pt_config* c, std::string* why) {
+  auto bad = [&](const std::string& s) {
+    *why = s;
+    return PT_EINVAL;
+  };
+  if (!c) return bad("null config");
+  if (c->n_layers < 1) return bad("n_layers must be >= 1");
+  if (!c->dims || !c->act || !c->stage_first_layer) return bad("dims/act/stage_first_layer must be set");
+  for (int i = 0; i <= c->n_layers; ++i)
+    if (c->dims[i] < 1) return bad("dims[" + std::to_string(i) + "] must be >= 1");
+  for (int i = 0; i < c->n_layers; ++i)
+    if (c->act[i] < PT_ACT_NONE || c->act[i] > PT_ACT_TANH)
+      return bad("act[" + std::to_string(i) + "] is not a PT_ACT_* value");
+  const int D = c->n_stages;
+  if (D < 1) return bad("n_stages must be >= 1");
+  if (D > c->n_layers)
+    return bad("D=" + std::to_string(D) + " > L=" + std::to_string(c->n_layers) + " (SPEC.md:151)");
+  const int32_t* b = c->stage_first_layer;
+  if (b[0] != 0 || b[D] != c->n_layers) return bad("stage plan must start at layer 0 and end at layer L");
+  for (int h = 0; h < D; ++h)
+    if (b[h] >= b[h + 1]) return bad("stage " + std::to_string(h + 1) + " is empty or out of order");
+  if (c->batch < 1 || c->batch > pt::MAXM) return bad("batch must be in [1, 16]");
+  for (int i = 0; i <= c->n_layers; ++i)
+    if (pad_dim(c->dims[i]) > pt::MAX_LD)
+      return bad("width " + std::to_string(c->dims[i]) + " exceeds the supported maximum 8192");
+  if (c->loss != PT_LOSS_MSE && c->loss != PT_LOSS_SOFTMAX_CE) return bad("unknown loss");
+  if (c->optimizer != PT_OPT_SGD && c->optimizer != PT_OPT_ADAM) return bad("unknown optimizer");
+  if (c->act_delay != 0 && c->act_delay != 1) return bad("act_delay must be 0 or 1");
+  if (c->local_stage_count < 0 || c->local_stage_first < 0 ||
+      c->local_stage_first + c->local_stage_count > D)
+    return bad("local stage range out of bounds");
+  return PT_OK;
+}
+
+int create_impl(const pt_config* c, pt_pipeline* p) {
+  std::string why;
+  if (validate(c, &why) != PT_OK) return fail(PT_EINVAL, why);
+  if (c->loss != PT_LOSS_MSE)
+    return fail(PT_EUNSUPPORTED, "softmax cross-entropy is not implemented on the B200 path");
+  if (c->optimizer != PT_OPT_SGD) return fail(PT_EUNSUPPORTED, "Adam is not implemented on the B200 path");
+  p->L = c->n_layers;
+  p->D = c->n_stages;
+  p->M = c->batch;
+  p->loss = c->loss;
+  p->opt = c->optimizer;
+  p->learn = c->learn ? 1 : 0;
+  p->act_delay = c->act_delay;
+  p->lr = c->lr;
+  p->dims.assign(c->dims, c->dims + p->L + 1);
+  p->act.assign(c->act, c->act + p->L);
+  p->sfl.assign(c->stage_first_layer, c->stage_first_layer + p->D + 1);
+  p->local_first = c->local_stage_count ? c->local_stage_first : 0;
+  p->local_count = c->local_stage_count ? c->local_stage_count : p->D;
+  p->timeout_ns = (unsigned long long)(c->timeout_ms > 0 ? c->timeout_ms : 30000) * 1000000ull;
+  p->fast = (p->M == 1);
+
+  CUDA_TRY(cudaGetDevice(&p->device));
+  int sms = 0, coop = 0;
+  CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device));
+  CUDA_TRY(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, p->device));
+  if (!coop) return fail(PT_EUNSUPPORTED, "device does not support cooperative launch");
+  CUDA_TRY(cudaFuncSetAttribute(pt::tick_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                int(pt::SMEM_BYTES)));
+  CUDA_TRY(cudaFuncSetAttribute(pt::tick_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                int(pt::SMEM_BYTES)));
+  int per_sm = 0;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pt::tick_kernel<true>, pt::NTHREADS,
+                                                         pt::SMEM_BYTES));
+  if (per_sm < 1) return fail(PT_EUNSUPPORTED, "tick kernel does not fit on one SM");
+  p->G = c->grid > 0 ? c->grid : sms;
+  if (p->G > sms * per_sm) return fail(PT_EINVAL, "grid exceeds co-resident CTA capacity");
+
+  // local layers
+  const int s_lo = p->local_first, s_hi = p->local_first + p->local_count;
+  p->layer_base = p->sfl[s_lo];
+  const int l_hi = p->sfl[s_hi];
+  for (int l = p->layer_base; l < l_hi; ++l) {
+    LayerHost Lh;
+    Lh.n_in = p->dims[l];
+    Lh.n_out = p->dims[l + 1];
+    Lh.ld_in = pad_dim(Lh.n_in);
+    Lh.ld_out = pad_dim(Lh.n_out);
+    Lh.act = p->act[l];
+    Lh.rows_per_chunk = pt::SLOT_FLOATS / Lh.ld_in;
+    const int max_rows = (Lh.n_out + p->G - 1) / p->G;
+    if (max_rows * p->M > pt::DELTA_FLOATS)
+      return fail(PT_EINVAL, "rows per CTA x batch exceeds the delta buffer; use a larger grid");
+    PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&Lh.W), size_t(Lh.n_out) * Lh.ld_in * 4));
+    PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&Lh.b), size_t(Lh.n_out) * 4));
+    p->layers.push_back(Lh);
+  }
+  // local stages
+  for (int s0 = s_lo; s0 < s_hi; ++s0) {
+    StageHost S;
+    S.h = s0 + 1;
+    S.first_global = p->sfl[s0];
+    S.k = p->sfl[s0 + 1] - p->sfl[s0];
+    S.first_local = S.first_global - p->layer_base;
+    S.ld0 = p->stage_ld0(s0);
+    S.ldk = p->stage_ldk(s0);
+    // cache slot: a_0 .. a_k, each [M][ld]
+    size_t off = 0;
+    for (int i = 0; i < S.k; ++i) {
+      LayerHost& Lh = p->layers[S.first_local + i];
+      Lh.cache_in = int(off);
+      off += size_t(p->M) * Lh.ld_in;
+      Lh.cache_out = int(off);
+    }
+    off += size_t(p->M) * p->layers[S.first_local + S.k - 1].ld_out;
+    S.cache_floats = align_up(off, 64);
+    PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&S.cache), 3 * S.cache_floats * 4));
+    PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&S.cnt), size_t(2 * S.k) * sizeof(u64)));
+    const CommLayout cl = p->layout_of(s0);
+    PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&S.comm), cl.total));
+    // g_in partials: needed by every layer except stage 1's first
+    if (p->learn) {
+      for (int i = 0; i < S.k; ++i) {
+        if (S.h == 1 && i == 0) continue;
+        LayerHost& Lh = p->layers[S.first_local + i];
+        for (int j = 0; j < 2; ++j)
+          PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&Lh.part[j]), size_t(p->G) * p->M * Lh.ld_in * 4));
+      }
+    }
+    p->stages.push_back(S);
+  }
+  // wire local neighbours
+  for (size_t s = 0; s < p->stages.size(); ++s) {
+    StageHost& S = p->stages[s];
+    if (s > 0) {
+      S.up = p->stages[s - 1].comm;
+      S.G_up = p->G;
+    }
+    if (s + 1 < p->stages.size()) {
+      S.down = p->stages[s + 1].comm;
+      S.G_down = p->G;
+    }
+  }
+  PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&p->d_layers), p->layers.size() * sizeof(pt::LayerDev)));
+  PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&p->d_stages), p->stages.size() * sizeof(pt::StageDev)));
+  PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&p->d_tick_end), sizeof(u64)));
+  PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&p->d_status), sizeof(int)));
+  PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&p->d_first_bad), sizeof(long long)));
+  const long long big = std::numeric_limits<long long>::max();
+  CUDA_TRY(cudaMemcpy(p->d_first_bad, &big, sizeof(big), cudaMemcpyHostToDevice));
+  p->yh = std::max(1, p->D);
+  if (p->has_last()) PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&p->yhist), size_t(p->yh) * p->M * p->F() * 4));
+  CUDA_TRY(cudaStreamCreateWithFlags(&p->own_stream, cudaStreamNonBlocking));
+  p->stream = p->own_stream;
+  CUDA_TRY(cudaEventCreate(&p->ev0));
+  CUDA_TRY(cudaEventCreate(&p->ev1));
+  PT_TRY(upload_desc(p));
+  CUDA_TRY(cudaDeviceSynchronize());
+  return PT_OK;
+}
+
+LayerHost* local_layer(pt_pipeline* p, int layer, std::string* why) {
+  const int li = layer - p->layer_base;
+  if (layer < 0 || layer >= p->L) {
+    *why = "layer index " + std::to_string(layer) + " out of range";
+    return nullptr;
+  }
+  if (li < 0 || li >= int(p->layers.size())) {
+    *why = "layer " + std::to_string(layer) + " is not owned by this process";
+    return nullptr;
+  }
+  return &p->layers[li];
+}
+
+int check_ready(pt_pipeline* p) {
+  if (p->broken) return fail(PT_ESTATE, "pipeline unusable after an earlier device-side failure");
+  for (const StageHost& S : p->stages) {
+    if (S.h > 1 && !S.up)
+      return fail(PT_EINVAL, "stage " + std::to_string(S.h) + ": upstream stage not imported (pt_ipc_import)");
+    if (S.h < p->D && !S.down)
+      return fail(PT_EINVAL, "stage " + std::to_string(S.h) + ": downstream stage not imported (pt_ipc_import)");
+  }
+  return PT_OK;
+}
+
+int read_status(pt_pipeline* p) {
+  int st = 0;
+  long long bad = 0;
+  CUDA_TRY(cudaMemcpy(&st, p->d_status, sizeof(int), cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(&bad, p->d_first_bad, sizeof(long long), cudaMemcpyDeviceToHost));
+  if (st != pt::ST_OK) {
+    p->broken = true;
+    return fail(PT_ETIMEOUT, "a stage waited longer than timeout_ms for a neighbour; pipeline state is lost");
+  }
+  if (bad != std::numeric_limits<long long>::max()) {
+    const long long big = std::numeric_limits<long long>::max();
+    CUDA_TRY(cudaMemcpy(p->d_first_bad, &big, sizeof(big), cudaMemcpyHostToDevice));
+    return fail(PT_ENONFINITE, "non-finite loss at step " + std::to_string(bad));
+  }
+  return PT_OK;
+}
+
+int run_impl(pt_pipeline* p, const float* xs, const float* ys, int64_t n, float* outs, float* losses,
+             uint8_t* valid, int where) {
+  PT_TRY(check_ready(p));
+  if (n <= 0) return PT_OK;
+  if (n > (1 << 30)) return fail(PT_EINVAL, "too many ticks in one call");
+  if (where != PT_HOST && where != PT_DEVICE) return fail(PT_EINVAL, "where must be PT_HOST or PT_DEVICE");
+  const cudaMemcpyKind h2d = where == PT_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+  const cudaMemcpyKind d2h = where == PT_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+  const int M = p->M, F = p->F();
+  const bool first = p->has_first(), last = p->has_last();
+  if (first && !xs) return fail(PT_EINVAL, "xs is required on the process that owns stage 1");
+  if (last && p->learn && !ys) return fail(PT_EINVAL, "targets are required for online learning (stage D)");
+  const int n0 = p->dims[0], ld0 = p->stage_ld0(0);
+
+  if (first) {
+    PT_TRY(ensure(p, &p->xs_pad, &p->xs_cap, size_t(n), size_t(M) * ld0));
+    CUDA_TRY(cudaMemcpy2DAsync(p->xs_pad, size_t(ld0) * 4, xs, size_t(n0) * 4, size_t(n0) * 4, size_t(n) * M,
+                               h2d, p->stream));
+  }
+  const float* ys_dev = nullptr;
+  float* outs_dev = nullptr;
+  float* losses_dev = nullptr;
+  uint8_t* valid_dev = nullptr;
+  if (last) {
+    if (ys) {
+      if (where == PT_HOST) {
+        PT_TRY(ensure(p, &p->ys_stage, &p->ys_cap, size_t(n), size_t(M) * F));
+        CUDA_TRY(cudaMemcpyAsync(p->ys_stage, ys, size_t(n) * M * F * 4, h2d, p->stream));
+        ys_dev = p->ys_stage;
+      } else {
+        ys_dev = ys;
+      }
+    }
+    if (where == PT_DEVICE && outs) {
+      outs_dev = outs;
+    } else {
+      PT_TRY(ensure(p, &p->outs_stage, &p->outs_cap, size_t(n), size_t(M) * F));
+      outs_dev = p->outs_stage;
+    }
+    PT_TRY(ensure(p, &p->loss_part, &p->lp_cap, size_t(n), size_t(p->G)));
+    if (where == PT_DEVICE) {
+      losses_dev = losses;
+      valid_dev = valid;
+    }
+    if (!losses_dev) {
+      PT_TRY(ensure(p, &p->losses_stage, &p->ls_cap, size_t(n), 1));
+      losses_dev = p->losses_stage;
+    }
+    if (!valid_dev) {
+      PT_TRY(ensure(p, &p->valid_stage, &p->vs_cap, size_t(n), 1));
+      valid_dev = p->valid_stage;
+    }
+  }
+
+  pt::Params P;
+  memset(&P, 0, sizeof(P));
+  P.stages = p->d_stages;
+  P.layers = p->d_layers;
+  P.n_stages = int(p->stages.size());
+  P.M = M;
+  P.D = p->D;
+  P.learn = p->learn;
+  P.act_delay = p->act_delay;
+  P.G = p->G;
+  P.F = F;
+  int nB = 0;
+  for (const StageHost& S : p->stages) nB += S.k;
+  P.nB = p->learn ? nB : 0;
+  P.lr = p->lr;
+  P.xs = first ? p->xs_pad : nullptr;
+  P.ys = ys_dev;
+  P.yhist = p->yhist;
+  P.yh = p->yh;
+  P.outs = outs_dev;
+  P.loss_part = last ? p->loss_part : nullptr;
+  P.t0 = p->t_next;
+  P.n = int(n);
+  P.tick_end = p->d_tick_end;
+  P.status = p->d_status;
+  P.timeout_ns = p->timeout_ns;
+
+  void* args[] = {&P};
+  CUDA_TRY(cudaEventRecord(p->ev0, p->stream));
+  if (p->fast)
+    CUDA_TRY(cudaLaunchCooperativeKernel((const void*)pt::tick_kernel<true>, dim3(p->G), dim3(pt::NTHREADS),
+                                         args, pt::SMEM_BYTES, p->stream));
+  else
+    CUDA_TRY(cudaLaunchCooperativeKernel((const void*)pt::tick_kernel<false>, dim3(p->G), dim3(pt::NTHREADS),
+                                         args, pt::SMEM_BYTES, p->stream));
+  CUDA_TRY(cudaEventRecord(p->ev1, p->stream));
+  p->timed = true;
+
+  if (last) {
+    const int threads = 256, warps_per_block = threads / 32;
+    const int blocks = int((n + warps_per_block - 1) / warps_per_block);
+    pt::epilogue_kernel<<<blocks, threads, 0, p->stream>>>(p->loss_part, p->G, int(n), p->t_next, p->D,
+                                                           1.f / float(M * F), ys_dev != nullptr ? 1 : 0,
+                                                           losses_dev, valid_dev, p->d_first_bad);
+    CUDA_TRY(cudaGetLastError());
+    // queue the last D-1 targets for the next call (target queue)
+    if (ys_dev) {
+      for (long long s = std::max<long long>(p->t_next, p->t_next + n - (p->D - 1)); s < p->t_next + n; ++s)
+        CUDA_TRY(cudaMemcpyAsync(p->yhist + size_t(s % p->yh) * M * F, ys_dev + size_t(s - p->t_next) * M * F,
+                                 size_t(M) * F * 4, cudaMemcpyDeviceToDevice, p->stream));
+    }
+    if (outs && outs != outs_dev)
+      CUDA_TRY(cudaMemcpyAsync(outs, outs_dev, size_t(n) * M * F * 4, d2h, p->stream));
+    if (losses && losses != losses_dev)
+      CUDA_TRY(cudaMemcpyAsync(losses, losses_dev, size_t(n) * 4, d2h, p->stream));
+    if (valid && valid != valid_dev)
+      CUDA_TRY(cudaMemcpyAsync(valid, valid_dev, size_t(n), d2h, p->stream));
+  }
+  p->t_next += n;
+  if (where == PT_HOST) {
+    CUDA_TRY(cudaStreamSynchronize(p->stream));
+    return read_status(p);
+  }
+  return PT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t pt_abi_version(void) { return PT_ABI_VERSION; }
+
+const char* pt_last_error(void) { return g_err.c_str(); }
+
+int pt_create(const pt_config* cfg, pt_pipeline** out) {
+  if (!out) return fail(PT_EINVAL, "out is null");
+  *out = nullptr;
+  pt_pipeline* p = new pt_pipeline();
+  int r = create_impl(cfg, p);
+  if (r != PT_OK) {
+    std::string keep = g_err;
+    pt_destroy(p);
+    g_err = keep;
+    return r;
+  }
+  *out = p;
+  return PT_OK;
+}
+
+void pt_destroy(pt_pipeline* p) {
+  if (!p) return;
+  cudaDeviceSynchronize();
+  for (void* q : p->ipc_opened) cudaIpcCloseMemHandle(q);
+  for (void* a : p->allocs)
+    if (a) cudaFree(a);
+  if (p->ev0) cudaEventDestroy(p->ev0);
+  if (p->ev1) cudaEventDestroy(p->ev1);
+  if (p->own_stream) cudaStreamDestroy(p->own_stream);
+  delete p;
+}
+
+int pt_set_params(pt_pipeline* p, int32_t layer, const float* W, const float* b, int32_t where) {
+  if (!p) return fail(PT_EINVAL, "null handle");
+  BusyGuard g(p);
+  if (!g.ok) return fail(PT_EBUSY, "contract violation: handle used concurrently");
+  std::string why;
+  LayerHost* Lh = local_layer(p, layer, &why);
+  if (!Lh) return fail(PT_EINVAL, why);
+  const cudaMemcpyKind k = where == PT_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+  CUDA_TRY(cudaStreamSynchronize(p->stream));
+  if (W)
+    CUDA_TRY(cudaMemcpy2D(Lh->W, size_t(Lh->ld_in) * 4, W, size_t(Lh->n_in) * 4, size_t(Lh->n_in) * 4,
+                          size_t(Lh->n_out), k));
+  if (b) CUDA_TRY(cudaMemcpy(Lh->b, b, size_t(Lh->n_out) * 4, k));
+  return PT_OK;
+}
+
+int pt_get_params(pt_pipeline* p, int32_t layer, float* W, float* b, int32_t where) {
+  if (!p) return fail(PT_EINVAL, "null handle");
+  BusyGuard g(p);
+  if (!g.ok) return fail(PT_EBUSY, "contract violation: extract called mid-step (SPEC.md:239)");
+  std::string why;
+  LayerHost* Lh = local_layer(p, layer, &why);
+  if (!Lh) return fail(PT_EINVAL, why);
+  const cudaMemcpyKind k = where == PT_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+  CUDA_TRY(cudaStreamSynchronize(p->stream));
+  if (W)
+    CUDA_TRY(cudaMemcpy2D(W, size_t(Lh->n_in) * 4, Lh->W, size_t(Lh->ld_in) * 4, size_t(Lh->n_in) * 4,
+                          size_t(Lh->n_out), k));
+  if (b) CUDA_TRY(cudaMemcpy(b, Lh->b, size_t(Lh->n_out) * 4, k));
+  return PT_OK;
+}
+
+int pt_run(pt_pipeline* p, const float* xs, const float* ys, int64_t n, float* outs, float* losses,
+           uint8_t* valid, int32_t where) {
+  if (!p) return fail(PT_EINVAL, "null handle");
+  BusyGuard g(p);
+  if (!g.ok) return fail(PT_EBUSY, "contract violation: pipeline_step called concurrently (SPEC.md:221)");
+  return run_impl(p, xs, ys, n, outs, losses, valid, where);
+}
+
+int pt_step(pt_pipeline* p, const float* x, const float* y, float* out, float* loss, int32_t* valid,
+            int32_t where) {
+  if (!p) return fail(PT_EINVAL, "null handle");
+  BusyGuard g(p);
+  if (!g.ok) return fail(PT_EBUSY, "contract violation: pipeline_step called concurrently (SPEC.md:221)");
+  uint8_t v8 = 0;
+  int r;
+  if (where == PT_HOST) {
+    r = run_impl(p, x, y, 1, out, loss, valid ? &v8 : nullptr, PT_HOST);
+    if (valid) *valid = v8;
+  } else {
+    // device I/O: valid is int32 on the caller side; go through the staging byte
+    r = run_impl(p, x, y, 1, out, loss, nullptr, PT_DEVICE);
+    if (r == PT_OK) {
+      if (cudaStreamSynchronize(p->stream) != cudaSuccess) return fail(PT_ECUDA, "stream sync failed");
+      r = read_status(p);
+      if (valid && p->has_last()) {
+        uint8_t hv = 0;
+        if (cudaMemcpy(&hv, p->valid_stage, 1, cudaMemcpyDeviceToHost) != cudaSuccess)
+          return fail(PT_ECUDA, "valid copy failed");
+        int32_t v32 = hv;
+        if (cudaMemcpy(valid, &v32, 4, cudaMemcpyHostToDevice) != cudaSuccess)
+          return fail(PT_ECUDA, "valid copy failed");
+      }
+    }
+  }
+  return r;
+}
+
+int pt_sync(pt_pipeline* p) {
+  if (!p) return fail(PT_EINVAL, "null handle");
+  BusyGuard g(p);
+  if (!g.ok) return fail(PT_EBUSY, "contract violation: handle used concurrently");
+  CUDA_TRY(cudaStreamSynchronize(p->stream));
+  return read_status(p);
+}
+
+int pt_set_stream(pt_pipeline* p, void* stream) {
+  if (!p) return fail(PT_EINVAL, "null handle");
+  CUDA_TRY(cudaStreamSynchronize(p->stream));
+  p->stream = stream ? reinterpret_cast<cudaStream_t>(stream) : p->own_stream;
+  return PT_OK;
+}
+
+int pt_last_kernel_ms(pt_pipeline* p, float* ms) {
+  if (!p || !ms) return fail(PT_EINVAL, "null argument");
+  if (!p->timed) return fail(PT_EINVAL, "no kernel has run yet");
+  CUDA_TRY(cudaEventSynchronize(p->ev1));
+  CUDA_TRY(cudaEventElapsedTime(ms, p->ev0, p->ev1));
+  return PT_OK;
+}
+
+int64_t pt_tick(pt_pipeline* p) { return p ? p->t_next : -1; }
+
+int pt_ipc_export(pt_pipeline* p, int32_t stage, void* buf, size_t cap, size_t* len) {
+  if (!p || !buf || !len) return fail(PT_EINVAL, "null argument");
+  if (cap < sizeof(IpcBlob)) return fail(PT_EINVAL, "buffer too small");
+  const int s = stage - 1 - p->local_first;
+  if (s < 0 || s >= int(p->stages.size())) return fail(PT_EINVAL, "stage is not local");
+  const StageHost& S = p->stages[s];
+  IpcBlob b;
+  memset(&b, 0, sizeof(b));
+  b.magic = PT_IPC_MAGIC;
+  b.abi = PT_ABI_VERSION;
+  b.stage = stage;
+  b.G = p->G;
+  b.M = p->M;
+  b.ld0 = S.ld0;
+  b.ldk = S.ldk;
+  b.comm_bytes = int64_t(p->layout_of(stage - 1).total);
+  CUDA_TRY(cudaIpcGetMemHandle(&b.handle, S.comm));
+  memcpy(buf, &b, sizeof(b));
+  *len = sizeof(b);
+  return PT_OK;
+}
+
+int pt_ipc_import(pt_pipeline* p, const void* buf, size_t len) {
+  if (!p || !buf) return fail(PT_EINVAL, "null argument");
+  if (len < sizeof(IpcBlob)) return fail(PT_EINVAL, "IPC blob too short");
+  IpcBlob b;
+  memcpy(&b, buf, sizeof(b));
+  if (b.magic != PT_IPC_MAGIC || b.abi != PT_ABI_VERSION) return fail(PT_EINVAL, "not a partime IPC blob");
+  const int s0 = b.stage - 1;
+  if (s0 < 0 || s0 >= p->D) return fail(PT_EINVAL, "IPC blob stage out of range");
+  if (b.M != p->M || b.ld0 != p->stage_ld0(s0) || b.ldk != p->stage_ldk(s0) ||
+      b.comm_bytes != int64_t(p->layout_of(s0).total))
+    return fail(PT_EINVAL, "IPC blob shape does not match this pipeline's config");
+  const int lo = p->local_first, hi = p->local_first + p->local_count;  // [lo, hi)
+  if (s0 >= lo && s0 < hi) return fail(PT_EINVAL, "stage is local; nothing to import");
+  if (s0 != lo - 1 && s0 != hi) return fail(PT_EINVAL, "stage is not a neighbour of the local stages");
+  void* ptr = nullptr;
+  CUDA_TRY(cudaIpcOpenMemHandle(&ptr, b.handle, cudaIpcMemLazyEnablePeerAccess));
+  p->ipc_opened.push_back(ptr);
+  if (s0 == lo - 1) {
+    p->stages.front().up = static_cast<char*>(ptr);
+    p->stages.front().G_up = b.G;
+  } else {
+    p->stages.back().down = static_cast<char*>(ptr);
+    p->stages.back().G_down = b.G;
+  }
+  return upload_desc(p);
+}
+
+}  // extern "C"

@@ -1,0 +1,100 @@
+"""partime.pipeline.Pipeline: the paper's wrapper around an nn.Sequential.
+
+    pipeline = Pipeline(net, sample_input, balance, devices, cuda_graph, loss_fn,
+                        sample_target, optim_settings)
+    for idx, (inp, target) in enumerate(stream):
+        pipeline.forward(inp, target)
+        if idx < len(pipeline.stages) - 1: continue     # warm-up
+        outputs, loss = pipeline.outputs_buffer, pipeline.loss_buffer
+
+Each forward() is one PARTIME tick (Alg. 1), executed by the
+persistent B200 tick kernel. The device-resident loop of pipeline_run replaces
+the paper's CUDA Graph capture. `cuda_graph` is accepted for signature
+compatibility and ignored.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+from ..engine import Pipeline as _Engine
+from ..model import StagePlan
+from .convert import sequential_to_model
+
+
+@dataclass
+class Stage:
+    index: int
+    modules: list
+    device: object
+
+
+class Pipeline:
+    def __init__(self, net, sample_input, balance, devices, cuda_graph=True, loss_fn=None,
+                 sample_target=None, optim_settings=None, act_delay=1):
+        import torch
+
+        if loss_fn is not None and not isinstance(loss_fn, torch.nn.MSELoss):
+            raise NotImplementedError("only torch.nn.MSELoss (mean) is implemented on the B200 path")
+        if loss_fn is not None and getattr(loss_fn, "reduction", "mean") != "mean":
+            raise NotImplementedError("MSELoss must use reduction='mean' (SPEC.md:74)")
+        lr = 1e-3
+        if optim_settings is not None:
+            cls, hp = optim_settings
+            if cls is not torch.optim.SGD:
+                raise NotImplementedError(f"optimizer {cls.__name__} is not implemented on the B200 path")
+            extra = {k: v for k, v in hp.items() if k not in ("lr",) and v not in (0, 0.0, False, None)}
+            if extra:
+                raise NotImplementedError(f"SGD options {sorted(extra)} are not implemented on the B200 path")
+            lr = float(hp.get("lr", lr))
+        devs = [torch.device(d) for d in devices] if devices else [torch.device("cuda", torch.cuda.current_device())]
+        if len({(d.type, d.index if d.index is not None else torch.cuda.current_device()) for d in devs}) != 1:
+            raise NotImplementedError("stages on several GPUs run one process per GPU "
+                                      "(paper_2210_09147_b200.dist.build_distributed); a single process "
+                                      "drives one device")
+        self.device = devs[0]
+        self.net = net
+        model = sequential_to_model(net)
+        plan = StagePlan.from_counts(list(balance))
+        si = sample_input.detach().cpu().numpy() if hasattr(sample_input, "detach") else sample_input
+        st = sample_target.detach().cpu().numpy() if hasattr(sample_target, "detach") else sample_target
+        with torch.cuda.device(self.device):
+            self._eng = _Engine(model, plan, "sgd", lr, si, st, act_delay=act_delay)
+        mods = list(net)
+        self.stages, a = [], 0
+        for h, c in enumerate(balance):
+            self.stages.append(Stage(h, mods[a:a + c], devs[min(h, len(devs) - 1)]))
+            a += c
+        shape = (self._eng.F,) if self._eng._squeeze else (self._eng.M, self._eng.F)
+        self.outputs_buffer = torch.zeros(shape, device=self.device)
+        self.loss_buffer = torch.zeros((), device=self.device)
+        self.cuda_graph = cuda_graph
+
+    def forward(self, inp, target=None):
+        """One tick: forward, push, delayed backward and update on every stage (Alg. 1)."""
+        import torch
+
+        inp = inp.to(self.device) if hasattr(inp, "to") else torch.as_tensor(inp, device=self.device)
+        if target is not None:
+            target = target.to(self.device) if hasattr(target, "to") else torch.as_tensor(target, device=self.device)
+        out = self._eng.step(inp, target)
+        self.outputs_buffer.copy_(out.output.reshape(self.outputs_buffer.shape))
+        if out.loss is not None:
+            self.loss_buffer.fill_(out.loss)
+        return out
+
+    __call__ = forward
+
+    def sync_to_net(self):
+        """Copy the pipeline's current weights back into the wrapped nn.Sequential."""
+        import torch
+
+        model = self._eng.extract_weights()
+        mods = list(self.net)
+        for mod, spec in zip(mods, model.layers):
+            if isinstance(mod, torch.nn.Linear):
+                with torch.no_grad():
+                    mod.weight.copy_(torch.from_numpy(spec.W))
+                    if mod.bias is not None:
+                        mod.bias.copy_(torch.from_numpy(spec.b))
+        return self.net

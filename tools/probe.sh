@@ -1,0 +1,3 @@
+nvidia-smi; nproc; lscpu | head -20; python -c "
+import torch; p=torch.cuda.get_device_properties(0); print(p); print('L2', p.L2_cache_size, 'SMs', p.multi_processor_count)
+" ; free -g
