@@ -119,6 +119,12 @@ int pt_last_kernel_ms(pt_pipeline* p, float* ms);
 /* Next global tick index (number of ticks executed so far). */
 int64_t pt_tick(pt_pipeline* p);
 
+/* Diagnostics (no reference counterpart): record device timestamps of one CTA's step
+ * phases during each run, (code << 56) | globaltimer ns. The first cap/2 entries hold
+ * consumer events, the rest producer events. cap = 0 turns tracing off. */
+int pt_set_trace(pt_pipeline* p, int32_t cta, int32_t cap);
+int pt_get_trace(pt_pipeline* p, uint64_t* out, int32_t cap);
+
 /* Multi-process (one process per GPU): export the inbound-slot block of a local stage
  * (a CUDA IPC handle plus shapes), and import a neighbour's block so the kernel can store
  * activations/gradients and ready flags straight into the peer's memory over NVLink. */

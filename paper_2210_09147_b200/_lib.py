@@ -31,7 +31,8 @@ PT_OPT = {"sgd": 0, "adam": 1}
 # every symbol include/partime_b200.h declares (checked by tests/test_capi.py)
 EXPORTS = (
     "pt_create", "pt_set_params", "pt_get_params", "pt_step", "pt_run", "pt_sync",
-    "pt_set_stream", "pt_last_kernel_ms", "pt_tick", "pt_ipc_export", "pt_ipc_import",
+    "pt_set_stream", "pt_last_kernel_ms", "pt_tick", "pt_set_trace", "pt_get_trace",
+    "pt_ipc_export", "pt_ipc_import",
     "pt_destroy", "pt_last_error", "pt_abi_version",
 )
 
@@ -100,12 +101,14 @@ def load():
     lib.pt_tick.restype = ctypes.c_int64
     lib.pt_ipc_export.argtypes = [P, ctypes.c_int32, P, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]
     lib.pt_ipc_import.argtypes = [P, P, ctypes.c_size_t]
+    lib.pt_set_trace.argtypes = [P, ctypes.c_int32, ctypes.c_int32]
+    lib.pt_get_trace.argtypes = [P, P, ctypes.c_int32]
     lib.pt_destroy.argtypes = [P]
     lib.pt_destroy.restype = None
     lib.pt_last_error.restype = ctypes.c_char_p
     lib.pt_abi_version.restype = ctypes.c_int32
     for name in ("pt_set_params", "pt_get_params", "pt_step", "pt_run", "pt_sync", "pt_set_stream",
-                 "pt_last_kernel_ms", "pt_ipc_export", "pt_ipc_import"):
+                 "pt_last_kernel_ms", "pt_ipc_export", "pt_ipc_import", "pt_set_trace", "pt_get_trace"):
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
     return lib

@@ -12,6 +12,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <string>
@@ -46,29 +47,27 @@ int fail(int code, const std::string& msg) {
 
 constexpr int32_t PT_IPC_MAGIC = 0x50544231;  // "PTB1"
 
-// Padded row stride: a power of two in [128, 1024], else a multiple of 2048. Each
-// 128-float segment then maps to one warp, and every column has a fixed owner thread.
+// Padded row stride: a power of two >= 128. A 32 KB chunk is then exactly 64
+// (row, 128-float segment) pairs, and every column has a fixed owner thread.
 int pad_dim(int n) {
-  if (n <= 128) return 128;
-  if (n <= 1024) {
-    int p = 128;
-    while (p < n) p <<= 1;
-    return p;
-  }
-  return (n + 2047) / 2048 * 2048;
+  int p = 128;
+  while (p < n) p <<= 1;
+  return p;
 }
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 // Comm block of one stage (lives on that stage's GPU). The layout is a pure function
 // of (M, ld0, ldk), so every process can address a neighbour's block from the config.
+// Slots hold tagged 8-byte words {value, tick tag}; the two credit counters sit on
+// separate 128-B lines.
 struct CommLayout {
-  static constexpr size_t IN_READY = 0, G_READY = 128, ACT_CREDIT = 256, G_CREDIT = 384, DATA = 512;
+  static constexpr size_t ACT_CREDIT = 0, G_CREDIT = 128, DATA = 256;
   size_t inslot_bytes = 0, gslot_bytes = 0, total = 0;
   CommLayout() = default;
   CommLayout(int M, int ld0, int ldk) {
-    inslot_bytes = align_up(size_t(M) * ld0 * 4, 256);
-    gslot_bytes = align_up(size_t(M) * ldk * 4, 256);
+    inslot_bytes = align_up(size_t(M) * ld0 * 8, 256);
+    gslot_bytes = align_up(size_t(M) * ldk * 8, 256);
     total = DATA + 2 * inslot_bytes + 2 * gslot_bytes;
   }
   size_t inslot(int p) const { return DATA + size_t(p) * inslot_bytes; }
@@ -85,7 +84,7 @@ struct LayerHost {
   int n_in = 0, n_out = 0, ld_in = 0, ld_out = 0, act = 0;
   float* W = nullptr;
   float* b = nullptr;
-  float* part[2] = {nullptr, nullptr};
+  u64* part[2] = {nullptr, nullptr};
   int rows_per_chunk = 0;
   int cache_in = 0, cache_out = 0;
 };
@@ -96,12 +95,12 @@ struct StageHost {
   int first_local = 0;          // index into the handle's layer array
   int ld0 = 0, ldk = 0;
   char* comm = nullptr;  // own comm block
-  float* cache = nullptr;
-  size_t cache_floats = 0;
-  u64* cnt = nullptr;
+  u64* cache = nullptr;  // 3 slots of tagged activations
+  size_t cache_words = 0;
   char* up = nullptr;    // upstream stage's comm block (local or IPC-mapped), h > 1
   char* down = nullptr;  // downstream stage's comm block, h < D
   int G_up = 0, G_down = 0;
+  bool up_remote = false, down_remote = false;
 };
 
 }  // namespace
@@ -144,6 +143,13 @@ struct pt_pipeline {
   std::atomic<int> busy{0};
   std::vector<void*> ipc_opened;
   std::vector<void*> allocs;
+  u64* d_trace = nullptr;
+  int trace_cap = 0, trace_cta = 0;
+  int pf_chunks = 0, split_bytes = 32768;  // tunables (env PT_PF_CHUNKS / PT_SPLIT_BYTES)
+  // shared-memory plan (see pt_kernels.cuh): ring slots first, then the small buffers
+  int nslot = 0, slot_floats = 0, qw = 0, act_off = 0, spart_off = 0, spart_floats = 0, delta_off = 0,
+      red_off = 0, scal_off = 0, bar_off = 0, flags_off = 0, smem_bytes = 0;
+  int dbg = 0;                                        // diagnostics (env PT_DBG)
 
   bool has_first() const { return local_first == 0; }
   bool has_last() const { return local_first + local_count == D; }
@@ -224,31 +230,28 @@ int upload_desc(pt_pipeline* p) {
     d.k = h.k;
     d.G_up = h.G_up;
     d.G_down = h.G_down;
+    d.up_remote = h.up_remote ? 1 : 0;
+    d.down_remote = h.down_remote ? 1 : 0;
     d.ld0 = h.ld0;
     d.ldk = h.ldk;
-    for (int j = 0; j < 3; ++j) d.cache[j] = h.cache + size_t(j) * h.cache_floats;
+    for (int j = 0; j < 3; ++j) d.cache[j] = h.cache + size_t(j) * h.cache_words;
     const CommLayout own = p->layout_of(s0);
     for (int j = 0; j < 2; ++j) {
-      d.inslot[j] = reinterpret_cast<float*>(h.comm + own.inslot(j));
-      d.gslot[j] = reinterpret_cast<float*>(h.comm + own.gslot(j));
+      d.inslot[j] = reinterpret_cast<u64*>(h.comm + own.inslot(j));
+      d.gslot[j] = reinterpret_cast<u64*>(h.comm + own.gslot(j));
     }
-    d.in_ready = reinterpret_cast<u64*>(h.comm + CommLayout::IN_READY);
-    d.g_ready = reinterpret_cast<u64*>(h.comm + CommLayout::G_READY);
     d.act_credit = reinterpret_cast<u64*>(h.comm + CommLayout::ACT_CREDIT);
     d.g_credit = reinterpret_cast<u64*>(h.comm + CommLayout::G_CREDIT);
     if (h.down) {
       const CommLayout dn = p->layout_of(s0 + 1);
-      for (int j = 0; j < 2; ++j) d.peer_inslot[j] = reinterpret_cast<float*>(h.down + dn.inslot(j));
-      d.peer_in_ready = reinterpret_cast<u64*>(h.down + CommLayout::IN_READY);
+      for (int j = 0; j < 2; ++j) d.peer_inslot[j] = reinterpret_cast<u64*>(h.down + dn.inslot(j));
       d.peer_g_credit = reinterpret_cast<u64*>(h.down + CommLayout::G_CREDIT);
     }
     if (h.up) {
       const CommLayout upl = p->layout_of(s0 - 1);
-      for (int j = 0; j < 2; ++j) d.peer_gslot[j] = reinterpret_cast<float*>(h.up + upl.gslot(j));
-      d.peer_g_ready = reinterpret_cast<u64*>(h.up + CommLayout::G_READY);
+      for (int j = 0; j < 2; ++j) d.peer_gslot[j] = reinterpret_cast<u64*>(h.up + upl.gslot(j));
       d.peer_act_credit = reinterpret_cast<u64*>(h.up + CommLayout::ACT_CREDIT);
     }
-    d.cnt = h.cnt;
   }
   CUDA_TRY(cudaMemcpy(p->d_layers, ld.data(), ld.size() * sizeof(pt::LayerDev), cudaMemcpyHostToDevice));
   CUDA_TRY(cudaMemcpy(p->d_stages, sd.data(), sd.size() * sizeof(pt::StageDev), cudaMemcpyHostToDevice));
@@ -289,6 +292,62 @@ int validate(const pt_config* c, std::string* why) {
   return PT_OK;
 }
 
+// Shared-memory plan: the ring gets every byte the small buffers do not need.
+int plan_smem(pt_pipeline* p) {
+  int max_ld = 128, maxrows = 1, sp_max = 1;
+  for (const LayerHost& Lh : p->layers) {
+    max_ld = std::max(max_ld, Lh.ld_in);
+    maxrows = std::max(maxrows, (Lh.n_out + p->G - 1) / p->G);
+  }
+  // 32 KB slots, 4 of them by default: measured best for the 2048-wide learning tick
+  // (profiles/round1_ring_sweep.md). Deeper rings only add queueing latency in front of
+  // the latency-critical activation/partial exchanges. PT_SLOT_KB / PT_NSLOT override.
+  int slot_bytes = 32768;
+  if (const char* e = getenv("PT_SLOT_KB"))
+    if (atoi(e) == 16 && max_ld <= 4096) slot_bytes = 16384;
+  p->slot_floats = slot_bytes / 4;
+  p->qw = p->slot_floats / (128 * pt::NCW);
+  int chunk_need = 0;
+  for (const LayerHost& Lh : p->layers) {
+    const int nseg = Lh.ld_in / 128;
+    const int sp = nseg >= p->qw ? nseg / p->qw : 1;
+    sp_max = std::max(sp_max, sp);
+    chunk_need = std::max(chunk_need, (p->slot_floats / Lh.ld_in) * sp * p->M);
+  }
+  const int layer_need = (maxrows * sp_max * p->M + 1) / 2;
+  p->spart_floats = std::max(chunk_need, std::min(layer_need, 4096));
+  const int delta_floats = p->M * maxrows;
+  const int act_floats = p->fast ? max_ld : 0;
+  auto a128 = [](size_t v) { return int(align_up(v, 128)); };
+  int off = 0;  // ring size decided last; lay out the tail from a fixed budget
+  const int tail = a128(size_t(act_floats) * 4) + a128(size_t(2 * p->spart_floats) * 4) +
+                   a128(size_t(delta_floats) * 4) + a128(size_t(pt::RED_FLOATS) * 4) + a128(64 * 4) +
+                   a128(2 * 16 * 8) + a128(16 * 4);
+  p->nslot = std::min(16, (pt::SMEM_MAX - tail) / slot_bytes);
+  int want = 4;
+  if (const char* e = getenv("PT_NSLOT")) want = std::max(2, atoi(e));
+  p->nslot = std::min(p->nslot, want);
+  if (p->nslot < 2)
+    return fail(PT_EINVAL, "shared memory too small for this layer shape (rows per CTA x batch); use a larger grid");
+  off = p->nslot * slot_bytes;
+  p->act_off = off;
+  off += a128(size_t(act_floats) * 4);
+  p->spart_off = off;
+  off += a128(size_t(2 * p->spart_floats) * 4);
+  p->delta_off = off;
+  off += a128(size_t(delta_floats) * 4);
+  p->red_off = off;
+  off += a128(size_t(pt::RED_FLOATS) * 4);
+  p->scal_off = off;
+  off += a128(64 * 4);
+  p->bar_off = off;
+  off += a128(2 * 16 * 8);
+  p->flags_off = off;
+  off += a128(16 * 4);
+  p->smem_bytes = off;
+  return PT_OK;
+}
+
 int create_impl(const pt_config* c, pt_pipeline* p) {
   std::string why;
   if (validate(c, &why) != PT_OK) return fail(PT_EINVAL, why);
@@ -310,19 +369,22 @@ int create_impl(const pt_config* c, pt_pipeline* p) {
   p->local_count = c->local_stage_count ? c->local_stage_count : p->D;
   p->timeout_ns = (unsigned long long)(c->timeout_ms > 0 ? c->timeout_ms : 30000) * 1000000ull;
   p->fast = (p->M == 1);
+  if (const char* e = getenv("PT_PF_CHUNKS")) p->pf_chunks = std::max(0, atoi(e));
+  if (const char* e = getenv("PT_DBG")) p->dbg = atoi(e);
+  if (const char* e = getenv("PT_SPLIT_BYTES")) p->split_bytes = std::max(1024, atoi(e)) / 16 * 16;
 
   CUDA_TRY(cudaGetDevice(&p->device));
   int sms = 0, coop = 0;
   CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device));
   CUDA_TRY(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, p->device));
   if (!coop) return fail(PT_EUNSUPPORTED, "device does not support cooperative launch");
-  CUDA_TRY(cudaFuncSetAttribute(pt::tick_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                int(pt::SMEM_BYTES)));
-  CUDA_TRY(cudaFuncSetAttribute(pt::tick_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                int(pt::SMEM_BYTES)));
+  CUDA_TRY(cudaFuncSetAttribute(pt::tick_kernel<true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, pt::SMEM_MAX));
+  CUDA_TRY(cudaFuncSetAttribute(pt::tick_kernel<true, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, pt::SMEM_MAX));
+  CUDA_TRY(cudaFuncSetAttribute(pt::tick_kernel<false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, pt::SMEM_MAX));
+  CUDA_TRY(cudaFuncSetAttribute(pt::tick_kernel<false, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, pt::SMEM_MAX));
   int per_sm = 0;
-  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pt::tick_kernel<true>, pt::NTHREADS,
-                                                         pt::SMEM_BYTES));
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pt::tick_kernel<true, 8>, pt::NTHREADS,
+                                                         pt::SMEM_MAX));
   if (per_sm < 1) return fail(PT_EUNSUPPORTED, "tick kernel does not fit on one SM");
   p->G = c->grid > 0 ? c->grid : sms;
   if (p->G > sms * per_sm) return fail(PT_EINVAL, "grid exceeds co-resident CTA capacity");
@@ -338,14 +400,12 @@ int create_impl(const pt_config* c, pt_pipeline* p) {
     Lh.ld_in = pad_dim(Lh.n_in);
     Lh.ld_out = pad_dim(Lh.n_out);
     Lh.act = p->act[l];
-    Lh.rows_per_chunk = pt::SLOT_FLOATS / Lh.ld_in;
-    const int max_rows = (Lh.n_out + p->G - 1) / p->G;
-    if (max_rows * p->M > pt::DELTA_FLOATS)
-      return fail(PT_EINVAL, "rows per CTA x batch exceeds the delta buffer; use a larger grid");
     PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&Lh.W), size_t(Lh.n_out) * Lh.ld_in * 4));
     PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&Lh.b), size_t(Lh.n_out) * 4));
     p->layers.push_back(Lh);
   }
+  PT_TRY(plan_smem(p));
+  for (LayerHost& Lh : p->layers) Lh.rows_per_chunk = p->slot_floats / Lh.ld_in;
   // local stages
   for (int s0 = s_lo; s0 < s_hi; ++s0) {
     StageHost S;
@@ -364,9 +424,8 @@ int create_impl(const pt_config* c, pt_pipeline* p) {
       Lh.cache_out = int(off);
     }
     off += size_t(p->M) * p->layers[S.first_local + S.k - 1].ld_out;
-    S.cache_floats = align_up(off, 64);
-    PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&S.cache), 3 * S.cache_floats * 4));
-    PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&S.cnt), size_t(2 * S.k) * sizeof(u64)));
+    S.cache_words = align_up(off, 64);
+    PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&S.cache), 3 * S.cache_words * sizeof(u64)));
     const CommLayout cl = p->layout_of(s0);
     PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&S.comm), cl.total));
     // g_in partials: needed by every layer except stage 1's first
@@ -375,7 +434,7 @@ int create_impl(const pt_config* c, pt_pipeline* p) {
         if (S.h == 1 && i == 0) continue;
         LayerHost& Lh = p->layers[S.first_local + i];
         for (int j = 0; j < 2; ++j)
-          PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&Lh.part[j]), size_t(p->G) * p->M * Lh.ld_in * 4));
+          PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&Lh.part[j]), size_t(p->G) * p->M * Lh.ld_in * sizeof(u64)));
       }
     }
     p->stages.push_back(S);
@@ -531,15 +590,29 @@ int run_impl(pt_pipeline* p, const float* xs, const float* ys, int64_t n, float*
   P.tick_end = p->d_tick_end;
   P.status = p->d_status;
   P.timeout_ns = p->timeout_ns;
+  P.nslot = p->nslot;
+  P.slot_floats = p->slot_floats;
+  P.act_off = p->act_off;
+  P.spart_off = p->spart_off;
+  P.spart_floats = p->spart_floats;
+  P.delta_off = p->delta_off;
+  P.red_off = p->red_off;
+  P.scal_off = p->scal_off;
+  P.bar_off = p->bar_off;
+  P.flags_off = p->flags_off;
+  P.pf_chunks = p->pf_chunks;
+  P.split_bytes = p->split_bytes;
+  P.dbg = p->dbg;
+  P.trace = p->d_trace;
+  P.trace_cap = p->trace_cap;
+  P.trace_cta = p->trace_cta;
+  if (p->d_trace) CUDA_TRY(cudaMemsetAsync(p->d_trace, 0, size_t(p->trace_cap) * sizeof(u64), p->stream));
 
   void* args[] = {&P};
   CUDA_TRY(cudaEventRecord(p->ev0, p->stream));
-  if (p->fast)
-    CUDA_TRY(cudaLaunchCooperativeKernel((const void*)pt::tick_kernel<true>, dim3(p->G), dim3(pt::NTHREADS),
-                                         args, pt::SMEM_BYTES, p->stream));
-  else
-    CUDA_TRY(cudaLaunchCooperativeKernel((const void*)pt::tick_kernel<false>, dim3(p->G), dim3(pt::NTHREADS),
-                                         args, pt::SMEM_BYTES, p->stream));
+  const void* fn = p->fast ? (p->qw == 8 ? (const void*)pt::tick_kernel<true, 8> : (const void*)pt::tick_kernel<true, 4>)
+                           : (p->qw == 8 ? (const void*)pt::tick_kernel<false, 8> : (const void*)pt::tick_kernel<false, 4>);
+  CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(p->G), dim3(pt::NTHREADS), args, size_t(p->smem_bytes), p->stream));
   CUDA_TRY(cudaEventRecord(p->ev1, p->stream));
   p->timed = true;
 
@@ -700,6 +773,30 @@ int pt_last_kernel_ms(pt_pipeline* p, float* ms) {
 
 int64_t pt_tick(pt_pipeline* p) { return p ? p->t_next : -1; }
 
+int pt_set_trace(pt_pipeline* p, int32_t cta, int32_t cap) {
+  if (!p) return fail(PT_EINVAL, "null handle");
+  CUDA_TRY(cudaStreamSynchronize(p->stream));
+  dev_free(p, p->d_trace);
+  p->d_trace = nullptr;
+  p->trace_cap = 0;
+  if (cap > 0) {
+    if (cta < 0 || cta >= p->G) return fail(PT_EINVAL, "trace CTA out of range");
+    PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&p->d_trace), size_t(cap) * sizeof(u64)));
+    p->trace_cap = cap;
+    p->trace_cta = cta;
+  }
+  return PT_OK;
+}
+
+int pt_get_trace(pt_pipeline* p, uint64_t* out, int32_t cap) {
+  if (!p || !out) return fail(PT_EINVAL, "null argument");
+  if (!p->d_trace) return fail(PT_EINVAL, "tracing is off (pt_set_trace)");
+  CUDA_TRY(cudaStreamSynchronize(p->stream));
+  const int n = std::min(cap, p->trace_cap);
+  CUDA_TRY(cudaMemcpy(out, p->d_trace, size_t(n) * sizeof(u64), cudaMemcpyDeviceToHost));
+  return PT_OK;
+}
+
 int pt_ipc_export(pt_pipeline* p, int32_t stage, void* buf, size_t cap, size_t* len) {
   if (!p || !buf || !len) return fail(PT_EINVAL, "null argument");
   if (cap < sizeof(IpcBlob)) return fail(PT_EINVAL, "buffer too small");
@@ -742,9 +839,11 @@ int pt_ipc_import(pt_pipeline* p, const void* buf, size_t len) {
   if (s0 == lo - 1) {
     p->stages.front().up = static_cast<char*>(ptr);
     p->stages.front().G_up = b.G;
+    p->stages.front().up_remote = true;
   } else {
     p->stages.back().down = static_cast<char*>(ptr);
     p->stages.back().G_down = b.G;
+    p->stages.back().down_remote = true;
   }
   return upload_desc(p);
 }

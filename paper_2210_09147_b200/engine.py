@@ -258,6 +258,19 @@ class Pipeline:
         _lib.check(self._lib.pt_last_kernel_ms(self._h, ctypes.byref(ms)), "last_kernel_ms")
         return float(ms.value)
 
+    def set_trace(self, cta=0, cap=1 << 16):
+        """Diagnostics: record device timestamps of one CTA's step phases (pt_set_trace)."""
+        _lib.check(self._lib.pt_set_trace(self._h, int(cta), int(cap)), "set_trace")
+        self._trace_cap = int(cap)
+
+    def get_trace(self):
+        """(consumer, producer) lists of (code, ns) from the last run."""
+        buf = np.zeros(self._trace_cap, np.uint64)
+        _lib.check(self._lib.pt_get_trace(self._h, _ptr(buf), self._trace_cap), "get_trace")
+        half, q = self._trace_cap // 2, self._trace_cap - self._trace_cap // 4
+        dec = lambda a: [(int(v >> np.uint64(56)), int(v & np.uint64(0x00FFFFFFFFFFFFFF))) for v in a if v]
+        return dec(buf[:half]), dec(buf[half:q]), dec(buf[q:])
+
     # ---- multi-process (one process per GPU) ----------------------------------------------
     def ipc_export(self, stage):
         buf = ctypes.create_string_buffer(256)
