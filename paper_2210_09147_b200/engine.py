@@ -223,11 +223,12 @@ class Pipeline:
         Returns (outs [n, M, F], losses [n], valid [n])."""
         n = int(n if n is not None else (xs.shape[0] if xs is not None else ys.shape[0]))
         M, F = self.M, self.F
-        dev = _is_cuda(xs) or _is_cuda(ys)
+        dev = _is_cuda(xs) or _is_cuda(ys) or (xs is None and ys is None and torch is not None)
         xs = None if xs is None else _f32(xs)
         ys = None if ys is None else _f32(ys)
         if dev:
-            d = xs.device if xs is not None else ys.device
+            d = xs.device if xs is not None else (ys.device if ys is not None else
+                                                   torch.device("cuda", torch.cuda.current_device()))
             outs = torch.empty((n, M, F), dtype=torch.float32, device=d)
             losses = torch.empty(n, dtype=torch.float32, device=d)
             valid = torch.empty(n, dtype=torch.uint8, device=d)

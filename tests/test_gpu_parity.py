@@ -79,3 +79,136 @@ def test_small_grid_uneven_rows():
 @pytest.mark.parametrize("M", [2, 4])
 def test_microbatch_generic(M):
     _case([32, 48, 40, 16], [2, 3], 25, 0.05, M=M)
+
+
+def _pipe(widths, counts, lr, M=1, seed=0, **kw):
+    m = mdl.mlp(widths, seed=seed)
+    st = streams.SmoothStream(widths[0], widths[-1], seed=seed + 1, batch=M)
+    return m, st, (lambda xs, ys: engine.Pipeline(m, counts, "sgd", lr, xs[0] if M > 1 else xs[0, 0],
+                                                  ys[0] if M > 1 else ys[0, 0], **kw))
+
+
+def test_step_api_matches_run():
+    """pipeline_step (per sample, host buffers) == pipeline_run (device-resident ring)."""
+    m, st, mk = _pipe([24, 40, 40, 12], [2, 3], 0.05)
+    xs, ys = st.block(0, 12)
+    xs, ys = xs.astype(np.float32), ys.astype(np.float32)
+    a, b = mk(xs, ys), mk(xs, ys)
+    outs, losses, valid = a.run(xs, ys)
+    for t in range(12):
+        o = b.step(xs[t, 0], ys[t, 0])
+        assert o.valid == bool(valid[t]) and o.source_sample_id == t - 1
+        assert np.array_equal(o.output, outs[t, 0])
+        if o.valid:
+            assert o.loss == float(losses[t])
+    for j in range(a.L):
+        assert all(np.array_equal(u, v) for u, v in zip(a.get_layer(j), b.get_layer(j)))
+
+
+def test_run_split_across_calls():
+    """Targets queued across pt_run calls: 3 calls == 1 call, bit for bit."""
+    m, st, mk = _pipe([16, 32, 32, 32, 8], [2, 2, 3], 0.05)
+    xs, ys = st.block(0, 15)
+    xs, ys = xs.astype(np.float32), ys.astype(np.float32)
+    a, b = mk(xs, ys), mk(xs, ys)
+    o1, l1, _ = a.run(xs, ys)
+    parts = [b.run(xs[i:j], ys[i:j]) for i, j in ((0, 4), (4, 5), (5, 15))]
+    assert np.array_equal(o1, np.concatenate([p[0] for p in parts]))
+    assert np.array_equal(l1, np.concatenate([p[1] for p in parts]), equal_nan=True)
+
+
+def test_deterministic_bitwise():
+    """Fixed reduction orders: two identical runs are bitwise identical."""
+    res = []
+    for _ in range(2):
+        m, st, mk = _pipe([64, 256, 256, 32], [2, 3], 0.02)
+        xs, ys = st.block(0, 10)
+        p = mk(xs, ys)
+        outs, losses, _ = p.run(xs.astype(np.float32), ys.astype(np.float32))
+        res.append((outs, losses, [p.get_layer(j) for j in range(p.L)]))
+    assert np.array_equal(res[0][0], res[1][0]) and np.array_equal(res[0][1], res[1][1], equal_nan=True)
+    for (Wa, ba), (Wb, bb) in zip(res[0][2], res[1][2]):
+        assert np.array_equal(Wa, Wb) and np.array_equal(ba, bb)
+
+
+def test_d4_single_gpu():
+    _case([48] * 9, [4, 4, 4, 3], 40, 0.02)
+
+
+def test_wide_layers_8192():
+    """ld = 8192 rows (one row per 32 KB chunk), as in config 5."""
+    _case([1024, 8192, 1024], [2, 1], 4, 1e-3)
+
+
+def test_c2_shape_short():
+    """Config 2 shapes (32 x 2048), D=1 and D=2, a few ticks against the f64 oracle."""
+    _case([2048] * 33, [63], 4, 1e-3)
+    _case([2048] * 33, [32, 31], 5, 1e-3)
+
+
+def test_microbatch_16():
+    """M=16 replay window (config 4 semantics) on the generic path."""
+    _case([64, 256, 128, 32], [2, 3], 12, 0.02, M=16)
+
+
+def test_nonfinite_loss_reports_step():
+    from paper_2210_09147_b200._lib import NonFiniteLoss
+    m, st, mk = _pipe([8, 16, 4], [2, 1], 0.01)
+    xs, ys = st.block(0, 6)
+    ys = ys.astype(np.float32)
+    ys[3] = np.inf
+    p = mk(xs, ys)
+    with pytest.raises(NonFiniteLoss, match="step 4"):
+        p.run(xs.astype(np.float32), ys)  # D=2: sample 3 is scored at step 4
+
+
+def test_extract_weights_versions():
+    m, st, mk = _pipe([8, 16, 16, 4], [2, 3], 0.01)
+    xs, ys = st.block(0, 7)
+    p = mk(xs, ys)
+    assert all(np.array_equal(a.W, b.W) for a, b in zip(p.extract_weights().dense_layers, m.dense_layers))
+    p.run(xs.astype(np.float32), ys.astype(np.float32))
+    w = p.extract_weights()
+    # stage h has applied updates at ticks t >= 2D-h-1 (SPEC.md:254): D=2 -> h=1 from t=2, h=2 from t=1
+    assert [l.version for l in w.layers if l.kind == "dense"] == [7 - 2, 7 - 1, 7 - 1]
+
+
+def test_lr0_leaves_weights_bit_identical():
+    m, st, mk = _pipe([8, 16, 16, 4], [2, 3], 0.0)
+    xs, ys = st.block(0, 9)
+    p = mk(xs, ys)
+    p.run(xs.astype(np.float32), ys.astype(np.float32))
+    for j, l in enumerate(m.dense_layers):
+        W, b = p.get_layer(j)
+        assert np.array_equal(W, l.W) and np.array_equal(b, l.b)
+
+
+def test_paper_pipeline_api():
+    """partime.pipeline.Pipeline over an nn.Sequential, driven like PAPER.md:663-671."""
+    import torch
+    from oracle import engine as oeng
+    from paper_2210_09147_b200.partime.balancing import balance_pipeline_partitions
+    from paper_2210_09147_b200.partime.pipeline import Pipeline as PaperPipeline
+    torch.manual_seed(0)
+    net = torch.nn.Sequential(torch.nn.Linear(12, 32), torch.nn.ReLU(), torch.nn.Linear(32, 32), torch.nn.Tanh(),
+                              torch.nn.Linear(32, 5))
+    balance = balance_pipeline_partitions(net, ["cuda:0", "cuda:0"], 2)
+    assert sum(balance) == 5 and len(balance) == 2
+    layers = [("dense", m.weight.detach().double().numpy().copy(), m.bias.detach().double().numpy().copy())
+              if isinstance(m, torch.nn.Linear) else (("relu",) if isinstance(m, torch.nn.ReLU) else ("tanh",))
+              for m in net]
+    bounds = [0, balance[0], 5]
+    st = streams.SmoothStream(12, 5, seed=2)
+    xs, ys = st.block(0, 10)
+    pipe = PaperPipeline(net, torch.zeros(12), balance, ["cuda:0", "cuda:0"], True, torch.nn.MSELoss(),
+                         torch.zeros(5), (torch.optim.SGD, {"lr": 0.05}))
+    ref = oeng.Pipeline(layers, bounds, 0.05, xs[0], ys[0])
+    for idx in range(10):
+        pipe.forward(torch.tensor(xs[idx, 0], dtype=torch.float32), torch.tensor(ys[idx, 0], dtype=torch.float32))
+        o = ref.step(xs[idx], ys[idx])
+        if idx < len(pipe.stages) - 1:
+            continue
+        assert np.allclose(pipe.outputs_buffer.cpu().numpy(), o.output[0], rtol=1e-4, atol=1e-6)
+        assert abs(float(pipe.loss_buffer) - o.loss) <= 1e-4 * max(1.0, o.loss)
+    pipe.sync_to_net()
+    assert np.allclose(net[0].weight.detach().numpy(), ref.extract_weights()[0][1], rtol=1e-4, atol=1e-6)
