@@ -148,7 +148,7 @@ struct pt_pipeline {
   int pf_chunks = 0, split_bytes = 32768;  // tunables (env PT_PF_CHUNKS / PT_SPLIT_BYTES)
   // shared-memory plan (see pt_kernels.cuh): ring slots first, then the small buffers
   int nslot = 0, slot_floats = 0, qw = 0, act_off = 0, spart_off = 0, spart_floats = 0, delta_off = 0,
-      red_off = 0, scal_off = 0, bar_off = 0, flags_off = 0, smem_bytes = 0;
+      red_off = 0, scal_off = 0, bar_off = 0, flags_off = 0, desc_off = 0, bias_off = 0, smem_bytes = 0;
   int dbg = 0;                                        // diagnostics (env PT_DBG)
 
   bool has_first() const { return local_first == 0; }
@@ -320,9 +320,15 @@ int plan_smem(pt_pipeline* p) {
   const int act_floats = p->fast ? max_ld : 0;
   auto a128 = [](size_t v) { return int(align_up(v, 128)); };
   int off = 0;  // ring size decided last; lay out the tail from a fixed budget
+  size_t bias_rows = 0;
+  for (const LayerHost& Lh : p->layers) bias_rows += (Lh.n_out + p->G - 1) / p->G;
+  const int n_stages_local = p->local_count;
+  const int desc_bytes = a128(p->layers.size() * sizeof(pt::LayerDev) + n_stages_local * sizeof(pt::StageDev) +
+                              p->layers.size() * sizeof(int));
+  const int bias_bytes = a128(bias_rows * 4);
   const int tail = a128(size_t(act_floats) * 4) + a128(size_t(2 * p->spart_floats) * 4) +
                    a128(size_t(delta_floats) * 4) + a128(size_t(pt::RED_FLOATS) * 4) + a128(64 * 4) +
-                   a128(2 * 16 * 8) + a128(16 * 4);
+                   a128(2 * 16 * 8) + a128(16 * 4) + desc_bytes + bias_bytes;
   p->nslot = std::min(16, (pt::SMEM_MAX - tail) / slot_bytes);
   int want = 4;
   if (const char* e = getenv("PT_NSLOT")) want = std::max(2, atoi(e));
@@ -344,7 +350,12 @@ int plan_smem(pt_pipeline* p) {
   off += a128(2 * 16 * 8);
   p->flags_off = off;
   off += a128(16 * 4);
+  p->desc_off = off;
+  off += desc_bytes;
+  p->bias_off = off;
+  off += bias_bytes;
   p->smem_bytes = off;
+  if (p->smem_bytes > pt::SMEM_MAX) return fail(PT_EINVAL, "shared-memory plan exceeds 227 KB");
   return PT_OK;
 }
 
@@ -600,6 +611,9 @@ int run_impl(pt_pipeline* p, const float* xs, const float* ys, int64_t n, float*
   P.scal_off = p->scal_off;
   P.bar_off = p->bar_off;
   P.flags_off = p->flags_off;
+  P.desc_off = p->desc_off;
+  P.bias_off = p->bias_off;
+  P.n_layers = int(p->layers.size());
   P.pf_chunks = p->pf_chunks;
   P.split_bytes = p->split_bytes;
   P.dbg = p->dbg;

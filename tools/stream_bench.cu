@@ -159,8 +159,13 @@ int main() {
              lbytes / (best * 1e-3) / 1e9, best * 1e3 / 32);
     };
     printf("layered + grid barrier per layer:\n");
-    runb(ring_kernel<4>, 4, 32768); runb(ring_kernel<5>, 5, 32768); runb(ring_kernel<6>, 6, 32768);
-    runb(ring_kernel<10>, 10, 16384); runb(ring_kernel<13>, 13, 16384);
+    for (int pfm : {0, 1, 2}) for (int pfd : {4, 8, 12, 20}) {
+      if (pfm == 0 && pfd != 4) continue;
+      cudaMemcpyToSymbol(g_pf_mode, &pfm, 4); cudaMemcpyToSymbol(g_pf_dist, &pfd, 4);
+      printf(" pf_mode=%d dist=%d:", pfm, pfd);
+      runb(ring_kernel<4>, 4, 32768);
+    }
+    { int zz0 = 0; cudaMemcpyToSymbol(g_pf_mode, &zz0, 4); }
     cudaMemcpyToSymbol(g_barrier, &z, 4); cudaMemcpyToSymbol(g_stall_ns, &z, 4);
   }
   for (int stall : {0}) for (int pfm : {0}) for (int pfd : {4}) {

@@ -5,8 +5,8 @@ import numpy as np, torch
 from collections import defaultdict
 from paper_2210_09147_b200 import engine, model as mdl, streams
 
-NAMES = {1: "F.begin", 2: "F.waited", 3: "F.act", 4: "F.chunks", 5: "F.arrived",
-         11: "B.begin", 12: "B.waited", 13: "B.delta+act", 14: "B.chunks", 15: "B.arrived", 20: "tick"}
+NAMES = {1: "F.begin", 2: "F.credit", 3: "F.input", 4: "F.chunks", 5: "F.end",
+         11: "B.begin", 12: "B.act", 13: "B.delta", 14: "B.chunks", 15: "B.push", 20: "tick"}
 
 def run(widths, D, learn=True, ticks=8, cta=0):
     m = mdl.mlp(widths, seed=0)
