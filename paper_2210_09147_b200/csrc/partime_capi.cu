@@ -794,7 +794,7 @@ int pt_set_trace(pt_pipeline* p, int32_t cta, int32_t cap) {
   p->d_trace = nullptr;
   p->trace_cap = 0;
   if (cap > 0) {
-    if (cta < 0 || cta >= p->G) return fail(PT_EINVAL, "trace CTA out of range");
+    if (cta < -1 || cta >= p->G) return fail(PT_EINVAL, "trace CTA out of range (-1 = all CTAs, step ends)");
     PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&p->d_trace), size_t(cap) * sizeof(u64)));
     p->trace_cap = cap;
     p->trace_cta = cta;

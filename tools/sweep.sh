@@ -1,2 +1,2 @@
-python -m pytest tests/test_gpu_parity.py -q -x 2>&1 | tail -2
-python tools/trace_probe.py one | grep -E "^==|->" | head -8
+for n in 4 5 6; do echo "NSLOT=$n: $(PT_NSLOT=$n python tools/trace_probe.py one | grep -E '^==')"; done
+PT_NSLOT=5 python tools/trace_probe.py one | grep -E "^==|->" | head -8
