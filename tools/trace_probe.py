@@ -46,6 +46,14 @@ def run(widths, D, learn=True, ticks=8, cta=0):
         print(f"  consumer inter-chunk gap (fwd) median {np.median(np.diff(ct)[[i-1 for i in fwd]])/1e3:.2f}us")
         rec = np.array([prod[i][1] - chunks[i - 5][1] for i in range(5, n)])
         print(f"  slot recycle (ready[c-5] -> issue[c]): median {np.median(rec)/1e3:.2f}us p90 {np.percentile(rec,90)/1e3:.2f}us")
+    if chunks:
+        bw = [(chunks[i + 1][1] - chunks[i][1]) for i in range(len(chunks) - 1) if chunks[i][0] == 8 and chunks[i + 1][0] == 7]
+        if bw:
+            bw = np.array(bw)
+            print(f"  backward chunk data wait: median {np.median(bw)/1e3:.2f}us p90 {np.percentile(bw,90)/1e3:.2f}us, "
+                  f"total {bw.sum()/1e3/ticks:.1f}us/tick over {len(bw)//ticks} chunks/tick")
+        b7 = [chunks[i][1] for i in range(len(chunks)) if chunks[i][0] == 7]
+        b8 = [chunks[i][1] for i in range(len(chunks)) if chunks[i][0] == 8]
     # a snippet of the raw timeline around tick 4
     base = cons[0][1]
     print("  first 40 events:", [(NAMES.get(c, c), round((t - base) / 1e3, 2)) for c, t in cons[:40]])
