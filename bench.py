@@ -53,6 +53,8 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("PT_BENCH_ONE_DEVICE"):  # test hook: all ranks share GPU 0 (time-sliced)
+        local = 0
     return rank, world, local
 
 
@@ -214,7 +216,10 @@ def main():
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if os.environ.get("PT_BENCH_ONE_DEVICE"):
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         gloo = dist.new_group(backend="gloo")
     D = max(world, 1)
     widths = [args.width] * (args.layers + 1)
@@ -321,6 +326,8 @@ def main():
     except Exception:
         peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
     tpt, ncu = load_traffic()
+    if ncu is None or ncu.get("config") != {"width": args.width, "layers": args.layers, "stages": D}:
+        tpt = None  # the committed capture is for another workload
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "traffic": (tpt * T if tpt else None),
             "kernel": "pt::tick_kernel", "algorithmic_bytes_per_launch": bytes_tick * T,
@@ -343,8 +350,9 @@ def main():
                     "sample_latency_ticks": D, "sample_latency_us": round(1e3 * total_ms / (args.steps * T) * D, 2)},
         "roofline": roof,
         "cpu_baseline": cpu,
-        "e2e": {"value": round(e2e_value, 2), "unit": "samples/s", "h2d_bytes_per_step": h2d if first else 0,
-                "d2h_bytes_per_step": d2h if last else 0},
+        # job-wide bytes: xs enter at stage 1's GPU, targets and results at stage D's
+        "e2e": {"value": round(e2e_value, 2), "unit": "samples/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
         "gpu_launches": 2 * args.steps,
         "clocks": clocks,
     }
