@@ -145,11 +145,12 @@ struct pt_pipeline {
   std::vector<void*> allocs;
   u64* d_trace = nullptr;
   int trace_cap = 0, trace_cta = 0;
-  int pf_chunks = 0, split_bytes = 32768;  // tunables (env PT_PF_CHUNKS / PT_SPLIT_BYTES)
+  int pf_chunks = 0, split_bytes = 32768, maxfly = 0;  // tunables (env PT_PF_CHUNKS / PT_SPLIT_BYTES)
   // shared-memory plan (see pt_kernels.cuh): ring slots first, then the small buffers
   int nslot = 0, slot_floats = 0, qw = 0, act_off = 0, spart_off = 0, spart_floats = 0, delta_off = 0,
       red_off = 0, scal_off = 0, bar_off = 0, flags_off = 0, desc_off = 0, bias_off = 0, smem_bytes = 0;
   int dbg = 0;                                        // diagnostics (env PT_DBG)
+  int policy = 0;                                     // weight-load L2 hint (env PT_POLICY)
 
   bool has_first() const { return local_first == 0; }
   bool has_last() const { return local_first + local_count == D; }
@@ -299,20 +300,25 @@ int plan_smem(pt_pipeline* p) {
     max_ld = std::max(max_ld, Lh.ld_in);
     maxrows = std::max(maxrows, (Lh.n_out + p->G - 1) / p->G);
   }
-  // 32 KB slots, 4 of them by default: measured best for the 2048-wide learning tick
-  // (profiles/round1_ring_sweep.md). Deeper rings only add queueing latency in front of
-  // the latency-critical activation/partial exchanges. PT_SLOT_KB / PT_NSLOT override.
-  int slot_bytes = 32768;
-  if (const char* e = getenv("PT_SLOT_KB"))
-    if (atoi(e) == 16 && max_ld <= 4096) slot_bytes = 16384;
+  // Ring geometry: 4 x 32 KB slots, measured best for the 2048-wide learning tick
+  // (profiles/round1_ring_sweep.md). 3 x 64 KB with one copy in flight per SM streams
+  // better in the stand-alone lock-step benchmark (tools/dep_bench.cu) but is slower in
+  // the tick kernel, where slots also carry the weight write-back (round 1 sweep).
+  // PT_SLOT_KB (16/32/64) / PT_NSLOT / PT_MAXFLY override.
+  int slot_kb = 32;
+  if (const char* e = getenv("PT_SLOT_KB")) slot_kb = atoi(e);
+  if (slot_kb != 16 && slot_kb != 32 && slot_kb != 64) slot_kb = 32;
+  if (slot_kb == 16 && max_ld > 4096) slot_kb = 32;
+  int slot_bytes = slot_kb * 1024;
   p->slot_floats = slot_bytes / 4;
-  p->qw = p->slot_floats / (128 * pt::NCW);
+  p->qw = slot_kb == 16 ? 4 : 8;  // a sub-chunk is NCW * qw (row, 128-float segment) pairs
+  const int sub_floats = 128 * pt::NCW * p->qw;
   int chunk_need = 0;
   for (const LayerHost& Lh : p->layers) {
     const int nseg = Lh.ld_in / 128;
     const int sp = nseg >= p->qw ? nseg / p->qw : 1;
     sp_max = std::max(sp_max, sp);
-    chunk_need = std::max(chunk_need, (p->slot_floats / Lh.ld_in) * sp * p->M);
+    chunk_need = std::max(chunk_need, std::max(1, sub_floats / Lh.ld_in) * sp * p->M);
   }
   const int layer_need = (maxrows * sp_max * p->M + 1) / 2;
   p->spart_floats = std::max(chunk_need, std::min(layer_need, 4096));
@@ -330,9 +336,18 @@ int plan_smem(pt_pipeline* p) {
                    a128(size_t(delta_floats) * 4) + a128(size_t(pt::RED_FLOATS) * 4) + a128(64 * 4) +
                    a128(2 * 16 * 8) + a128(16 * 4) + desc_bytes + bias_bytes;
   p->nslot = std::min(16, (pt::SMEM_MAX - tail) / slot_bytes);
-  int want = 4;
+  if (p->nslot < 3 && slot_kb == 64) {
+    slot_kb = 32;
+    slot_bytes = 32768;
+    p->slot_floats = slot_bytes / 4;
+    p->nslot = std::min(16, (pt::SMEM_MAX - tail) / slot_bytes);
+  }
+  int want = slot_kb == 64 ? 3 : 4;
   if (const char* e = getenv("PT_NSLOT")) want = std::max(2, atoi(e));
   p->nslot = std::min(p->nslot, want);
+  p->maxfly = slot_kb == 64 ? 1 : 0;
+  if (const char* e = getenv("PT_MAXFLY")) p->maxfly = std::max(0, atoi(e));
+  if (!getenv("PT_SPLIT_BYTES")) p->split_bytes = slot_bytes;
   if (p->nslot < 2)
     return fail(PT_EINVAL, "shared memory too small for this layer shape (rows per CTA x batch); use a larger grid");
   off = p->nslot * slot_bytes;
@@ -382,6 +397,7 @@ int create_impl(const pt_config* c, pt_pipeline* p) {
   p->fast = (p->M == 1);
   if (const char* e = getenv("PT_PF_CHUNKS")) p->pf_chunks = std::max(0, atoi(e));
   if (const char* e = getenv("PT_DBG")) p->dbg = atoi(e);
+  if (const char* e = getenv("PT_POLICY")) p->policy = atoi(e);
   if (const char* e = getenv("PT_SPLIT_BYTES")) p->split_bytes = std::max(1024, atoi(e)) / 16 * 16;
 
   CUDA_TRY(cudaGetDevice(&p->device));
@@ -616,7 +632,9 @@ int run_impl(pt_pipeline* p, const float* xs, const float* ys, int64_t n, float*
   P.n_layers = int(p->layers.size());
   P.pf_chunks = p->pf_chunks;
   P.split_bytes = p->split_bytes;
+  P.maxfly = p->maxfly;
   P.dbg = p->dbg;
+  P.policy = p->policy;
   P.trace = p->d_trace;
   P.trace_cap = p->trace_cap;
   P.trace_cta = p->trace_cta;
