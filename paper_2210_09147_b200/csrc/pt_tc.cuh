@@ -1,0 +1,153 @@
+// pt_tc.cuh: sm_100a tensor-core building blocks (tcgen05 kind::tf32, TMEM, TMA 2-D tensor
+// copies) for the micro-batch tile kernel, plus the host-side tensor-map encoder.
+//
+// Operand layouts (UMMA shared-memory descriptors, version 1):
+//   - K-major SWIZZLE_128B: a TMA box of [rows][32 fp32] with CU_TENSOR_MAP_SWIZZLE_128B;
+//     8-row atoms of 1024 B (SBO), the K-step (8 tf32 = 32 B) advances the start address.
+//   - MN-major SWIZZLE_128B_BASE32B: a TMA box of [K rows][32 fp32 of MN] with
+//     CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B; 4-row K groups of 512 B (SBO), 32-element MN
+//     groups at LBO (one box apart). MN-major tf32 accepts only this layout.
+//   - K-major no swizzle: core matrices of 8 rows x 16 B, K-adjacent cores 128 B apart
+//     (LBO), 8-row groups (K/4)*128 B apart (SBO). Written by SIMT code (small operands).
+// Verified bit-exactly on B200 by tools/tc_probe2.cu.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "pt_ptx.cuh"
+
+namespace pt {
+
+// ------------------------------------------------------------- descriptors
+__host__ __device__ __forceinline__ uint32_t tc_idesc_tf32(int M, int N, bool a_mn, bool b_mn) {
+  uint32_t d = 0;
+  d |= 1u << 4;   // D format f32
+  d |= 2u << 7;   // A format tf32
+  d |= 2u << 10;  // B format tf32
+  d |= uint32_t(a_mn) << 15;
+  d |= uint32_t(b_mn) << 16;
+  d |= uint32_t(N >> 3) << 17;
+  d |= uint32_t(M >> 4) << 24;
+  return d;
+}
+
+__device__ __forceinline__ uint64_t tc_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
+  uint64_t d = 0;
+  d |= uint64_t((saddr >> 4) & 0x3FFF);
+  d |= uint64_t((lbo >> 4) & 0x3FFF) << 16;
+  d |= uint64_t((sbo >> 4) & 0x3FFF) << 32;
+  d |= uint64_t(1) << 46;  // version (sm100)
+  d |= uint64_t(layout & 7) << 61;
+  return d;
+}
+
+// byte offset of element (row, k) of a [rows][K] operand in the no-swizzle K-major layout
+__host__ __device__ __forceinline__ uint32_t tc_kmajor_noswz_off(int row, int k, int K) {
+  return uint32_t((row >> 3) * (K >> 2) * 128 + (k >> 2) * 128 + (row & 7) * 16 + (k & 3) * 4);
+}
+// descriptor of K-step ks (8 tf32) of such an operand
+__device__ __forceinline__ uint64_t tc_desc_kmajor_noswz(const void* base, int ks, int K) {
+  return tc_desc(smem_u32(base) + uint32_t(ks) * 256u, 128u, uint32_t(K >> 2) * 128u, 0u);
+}
+// K-major SWIZZLE_128B tile (1024-B aligned); kbyte = 32 * (K-step within the 32-float box)
+__device__ __forceinline__ uint64_t tc_desc_kmajor_sw128(const void* tile, uint32_t kbyte) {
+  return tc_desc(smem_u32(tile) + kbyte, 16u, 1024u, 2u);
+}
+// MN-major SWIZZLE_128B_BASE32B tile: boxes of [K rows][32 MN] lbo bytes apart, K rows of 128 B
+__device__ __forceinline__ uint64_t tc_desc_mn_sw128b32(const void* tile, int krow0, uint32_t lbo) {
+  return tc_desc(smem_u32(tile) + uint32_t(krow0) * 128u, lbo, 512u, 1u);
+}
+
+// ------------------------------------------------------------- tcgen05 ops
+__device__ __forceinline__ void tc_mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, bool acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(uint32_t(acc)));
+}
+// arrive on an mbarrier once every tcgen05 op this thread issued so far has completed
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// warp-wide: allocate ncols TMEM columns, base address written to smem
+__device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+               "r"(ncols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_free(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+// warp-wide: lane i gets TMEM lane (taddr.lane + i), 16 consecutive 32-bit columns
+__device__ __forceinline__ void tmem_ld_32x32b_x16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_ld_32x32b_x32(uint32_t taddr, float (&v)[32]) {
+  float a[16], b[16];
+  tmem_ld_32x32b_x16(taddr, a);
+  tmem_ld_32x32b_x16(taddr + 16, b);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    v[i] = a[i];
+    v[16 + i] = b[i];
+  }
+}
+
+// ------------------------------------------------------------- TMA 2-D
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+          "r"(smem_u32(dst)),
+      "l"(tm), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* tm, const void* src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%1, %2}], [%3];" ::"l"(tm), "r"(c0),
+               "r"(c1), "r"(smem_u32(src))
+               : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* tm) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(tm) : "memory");
+}
+
+// ------------------------------------------------------------- host: tensor maps
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// 2-D fp32 tensor [rows][cols] (row pitch ld_cols floats), box [box_rows][box_cols]; 0 = ok
+static inline int tc_make_tmap_2d(CUtensorMap* tm, const float* base, int cols, int rows, int box_cols, int box_rows,
+                                  CUtensorMapSwizzle swz, int ld_cols = 0) {
+  static PFN_encodeTiled fn = nullptr;
+  if (fn == nullptr) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess || p == nullptr)
+      return -1;
+    fn = reinterpret_cast<PFN_encodeTiled>(p);
+  }
+  const cuuint64_t dims[2] = {cuuint64_t(cols), cuuint64_t(rows)};
+  const cuuint64_t strides[1] = {cuuint64_t(ld_cols > 0 ? ld_cols : cols) * 4};
+  const cuuint32_t box[2] = {cuuint32_t(box_cols), cuuint32_t(box_rows)};
+  const cuuint32_t es[2] = {1, 1};
+  CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : int(r);
+}
+
+}  // namespace pt
