@@ -119,6 +119,14 @@ int pt_last_kernel_ms(pt_pipeline* p, float* ms);
 /* Next global tick index (number of ticks executed so far). */
 int64_t pt_tick(pt_pipeline* p);
 
+/* Which device path the handle runs (no reference counterpart; the engine picks it at
+ * pt_create): PT_PATH_TICK = per-row SIMT tick kernel (any shape, one process per GPU),
+ * PT_PATH_TILE = tcgen05 tensor-core tile kernel (batch 16, widths % 256 == 0, all stages
+ * in this process; set PT_TILE=0 in the environment to disable). Negative = error. */
+#define PT_PATH_TICK 0
+#define PT_PATH_TILE 1
+int32_t pt_kernel_path(const pt_pipeline* p);
+
 /* Diagnostics (no reference counterpart): record device timestamps of one CTA's step
  * phases during each run, (code << 56) | globaltimer ns. The first cap/2 entries hold
  * consumer events, the rest producer events. cap = 0 turns tracing off. */

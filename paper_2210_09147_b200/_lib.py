@@ -32,7 +32,7 @@ PT_OPT = {"sgd": 0, "adam": 1}
 EXPORTS = (
     "pt_create", "pt_set_params", "pt_get_params", "pt_step", "pt_run", "pt_sync",
     "pt_set_stream", "pt_last_kernel_ms", "pt_tick", "pt_set_trace", "pt_get_trace",
-    "pt_ipc_export", "pt_ipc_import",
+    "pt_ipc_export", "pt_ipc_import", "pt_kernel_path",
     "pt_destroy", "pt_last_error", "pt_abi_version",
 )
 
@@ -99,6 +99,8 @@ def load():
     lib.pt_last_kernel_ms.argtypes = [P, f32p]
     lib.pt_tick.argtypes = [P]
     lib.pt_tick.restype = ctypes.c_int64
+    lib.pt_kernel_path.argtypes = [P]
+    lib.pt_kernel_path.restype = ctypes.c_int32
     lib.pt_ipc_export.argtypes = [P, ctypes.c_int32, P, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]
     lib.pt_ipc_import.argtypes = [P, P, ctypes.c_size_t]
     lib.pt_set_trace.argtypes = [P, ctypes.c_int32, ctypes.c_int32]

@@ -20,6 +20,7 @@
 
 #include "partime_b200.h"
 #include "pt_kernels.cuh"
+#include "pt_tile.cuh"
 
 using pt::u64;
 
@@ -101,6 +102,12 @@ struct StageHost {
   char* down = nullptr;  // downstream stage's comm block, h < D
   int G_up = 0, G_down = 0;
   bool up_remote = false, down_remote = false;
+  // micro-batch tile path (plain fp32 buffers): cache[2] slots of a_0..a_k, inslot[2], gslot[2]
+  float* tcache = nullptr;
+  size_t tcache_floats = 0;
+  float* tin = nullptr;  // [2][M][n0]
+  float* tg = nullptr;   // [2][M][nk]
+  int n0 = 0, nk = 0;
 };
 
 }  // namespace
@@ -150,6 +157,15 @@ struct pt_pipeline {
   int nslot = 0, slot_floats = 0, qw = 0, act_off = 0, spart_off = 0, spart_floats = 0, delta_off = 0,
       red_off = 0, scal_off = 0, bar_off = 0, flags_off = 0, desc_off = 0, bias_off = 0, smem_bytes = 0;
   int dbg = 0;                                        // diagnostics (env PT_DBG)
+  // micro-batch tensor-core path (pt_tile.cuh): M == 16, widths % 256 == 0, single process
+  bool tile = false;
+  int t_smem = 0, t_maxn = 0;
+  float* t_part = nullptr;
+  float* t_delta = nullptr;
+  u64* t_bars = nullptr;  // [0] grid barrier, [16] weight write-back counter
+  CUtensorMap* d_tmaps = nullptr;
+  pt::TLayer* d_tlayers = nullptr;
+  pt::TStage* d_tstages = nullptr;
   int policy = 0;                                     // weight-load L2 hint (env PT_POLICY)
 
   bool has_first() const { return local_first == 0; }
@@ -374,6 +390,79 @@ int plan_smem(pt_pipeline* p) {
   return PT_OK;
 }
 
+// Buffers, tensor maps and descriptors of the micro-batch tile path (pt_tile.cuh).
+int setup_tile(pt_pipeline* p) {
+  const int M = p->M;
+  int maxn = 0;
+  for (int i = 0; i <= p->L; ++i) maxn = std::max(maxn, p->dims[i]);
+  p->t_maxn = maxn;
+  PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&p->t_part), size_t(pt::T_Q) * M * maxn * 4));
+  PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&p->t_delta), size_t(M) * maxn * 4));
+  PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&p->t_bars), 32 * sizeof(u64)));
+  std::vector<CUtensorMap> maps(2 * p->layers.size());
+  std::vector<pt::TLayer> tl(p->layers.size());
+  PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&p->d_tmaps), maps.size() * sizeof(CUtensorMap)));
+  for (size_t i = 0; i < p->layers.size(); ++i) {
+    const LayerHost& Lh = p->layers[i];
+    if (pt::tc_make_tmap_2d(&maps[2 * i], Lh.W, Lh.n_in, Lh.n_out, 32, 128, CU_TENSOR_MAP_SWIZZLE_128B, Lh.ld_in) ||
+        pt::tc_make_tmap_2d(&maps[2 * i + 1], Lh.W, Lh.n_in, Lh.n_out, 32, 64, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
+                            Lh.ld_in))
+      return fail(PT_ECUDA, "cuTensorMapEncodeTiled failed for layer " + std::to_string(p->layer_base + i));
+    tl[i].tmf = p->d_tmaps + 2 * i;
+    tl[i].tmb = p->d_tmaps + 2 * i + 1;
+    tl[i].b = Lh.b;
+    tl[i].n_in = Lh.n_in;
+    tl[i].n_out = Lh.n_out;
+    tl[i].act = Lh.act;
+  }
+  std::vector<pt::TStage> ts(p->stages.size());
+  for (size_t s = 0; s < p->stages.size(); ++s) {
+    StageHost& S = p->stages[s];
+    S.n0 = p->dims[S.first_global];
+    S.nk = p->dims[S.first_global + S.k];
+    size_t off = 0;
+    for (int i = 0; i < S.k; ++i) {
+      pt::TLayer& t = tl[S.first_local + i];
+      t.a_in = int(off);
+      off += size_t(M) * t.n_in;
+      t.a_out = int(off);
+    }
+    off += size_t(M) * S.nk;
+    S.tcache_floats = align_up(off, 64);
+    PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&S.tcache), 2 * S.tcache_floats * 4));
+    PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&S.tin), 2 * size_t(M) * S.n0 * 4));
+    PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&S.tg), 2 * size_t(M) * S.nk * 4));
+  }
+  for (size_t s = 0; s < p->stages.size(); ++s) {
+    StageHost& S = p->stages[s];
+    pt::TStage& d = ts[s];
+    memset(&d, 0, sizeof(d));
+    d.h = S.h;
+    d.first = S.first_local;
+    d.k = S.k;
+    d.n0 = S.n0;
+    d.nk = S.nk;
+    for (int j = 0; j < 2; ++j) {
+      d.cache[j] = S.tcache + size_t(j) * S.tcache_floats;
+      d.inslot[j] = S.tin + size_t(j) * M * S.n0;
+      d.gslot[j] = S.tg + size_t(j) * M * S.nk;
+      if (s + 1 < p->stages.size()) d.down_inslot[j] = p->stages[s + 1].tin + size_t(j) * M * p->stages[s + 1].n0;
+      if (s > 0) d.up_gslot[j] = p->stages[s - 1].tg + size_t(j) * M * p->stages[s - 1].nk;
+    }
+  }
+  PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&p->d_tlayers), tl.size() * sizeof(pt::TLayer)));
+  PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&p->d_tstages), ts.size() * sizeof(pt::TStage)));
+  CUDA_TRY(cudaMemcpy(p->d_tmaps, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(p->d_tlayers, tl.data(), tl.size() * sizeof(pt::TLayer), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(p->d_tstages, ts.data(), ts.size() * sizeof(pt::TStage), cudaMemcpyHostToDevice));
+  // shared memory: 1 KB alignment slack, ring, lo, operands, delta tile, reductions, barriers
+  p->t_smem = 1024 + (pt::T_NSLOT + 2) * pt::T_SLOT_FLOATS * 4 + 2 * 2 * M * pt::T_CK * 4 + pt::T_CK * M * 4 + 64 +
+              (2 * pt::T_NSLOT + 6) * 8 + 16;
+  if (p->t_smem > pt::SMEM_MAX) return fail(PT_EINVAL, "tile path shared-memory plan exceeds 227 KB");
+  CUDA_TRY(cudaFuncSetAttribute(pt::tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, p->t_smem));
+  return PT_OK;
+}
+
 int create_impl(const pt_config* c, pt_pipeline* p) {
   std::string why;
   if (validate(c, &why) != PT_OK) return fail(PT_EINVAL, why);
@@ -415,6 +504,18 @@ int create_impl(const pt_config* c, pt_pipeline* p) {
   if (per_sm < 1) return fail(PT_EUNSUPPORTED, "tick kernel does not fit on one SM");
   p->G = c->grid > 0 ? c->grid : sms;
   if (p->G > sms * per_sm) return fail(PT_EINVAL, "grid exceeds co-resident CTA capacity");
+  {
+    // micro-batch tensor-core path: every width a multiple of 256, M == 16, all stages here
+    bool ok = p->M == 16 && p->local_count == p->D && p->opt == PT_OPT_SGD && p->loss == PT_LOSS_MSE;
+    int units = 0;
+    for (int i = 0; i <= p->L && ok; ++i) ok = (p->dims[i] % 256) == 0;
+    for (int i = 0; i < p->L && ok; ++i) units = std::max(units, std::max(p->dims[i + 1], p->dims[i]) / 128 * pt::T_Q);
+    if (const char* e = getenv("PT_TILE")) ok = ok && atoi(e) != 0;
+    if (ok && c->grid <= 0) {
+      p->tile = true;
+      p->G = std::min(sms, units);
+    }
+  }
 
   // local layers
   const int s_lo = p->local_first, s_hi = p->local_first + p->local_count;
@@ -456,7 +557,7 @@ int create_impl(const pt_config* c, pt_pipeline* p) {
     const CommLayout cl = p->layout_of(s0);
     PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&S.comm), cl.total));
     // g_in partials: needed by every layer except stage 1's first
-    if (p->learn) {
+    if (p->learn && !p->tile) {
       for (int i = 0; i < S.k; ++i) {
         if (S.h == 1 && i == 0) continue;
         LayerHost& Lh = p->layers[S.first_local + i];
@@ -491,6 +592,7 @@ int create_impl(const pt_config* c, pt_pipeline* p) {
   p->stream = p->own_stream;
   CUDA_TRY(cudaEventCreate(&p->ev0));
   CUDA_TRY(cudaEventCreate(&p->ev1));
+  if (p->tile) PT_TRY(setup_tile(p));
   PT_TRY(upload_desc(p));
   CUDA_TRY(cudaDeviceSynchronize());
   return PT_OK;
@@ -640,12 +742,49 @@ int run_impl(pt_pipeline* p, const float* xs, const float* ys, int64_t n, float*
   P.trace_cta = p->trace_cta;
   if (p->d_trace) CUDA_TRY(cudaMemsetAsync(p->d_trace, 0, size_t(p->trace_cap) * sizeof(u64), p->stream));
 
-  void* args[] = {&P};
-  CUDA_TRY(cudaEventRecord(p->ev0, p->stream));
-  const void* fn = p->fast ? (p->qw == 8 ? (const void*)pt::tick_kernel<true, 8> : (const void*)pt::tick_kernel<true, 4>)
-                           : (p->qw == 8 ? (const void*)pt::tick_kernel<false, 8> : (const void*)pt::tick_kernel<false, 4>);
-  CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(p->G), dim3(pt::NTHREADS), args, size_t(p->smem_bytes), p->stream));
-  CUDA_TRY(cudaEventRecord(p->ev1, p->stream));
+  if (p->tile) {
+    pt::TParams T;
+    memset(&T, 0, sizeof(T));
+    T.stages = p->d_tstages;
+    T.layers = p->d_tlayers;
+    T.n_stages = int(p->stages.size());
+    T.M = M;
+    T.D = p->D;
+    T.learn = p->learn;
+    T.act_delay = p->act_delay;
+    T.F = F;
+    T.G = p->G;
+    T.lr = p->lr;
+    T.xs = p->xs_pad;
+    T.ldx = ld0;
+    T.ys = ys_dev;
+    T.yhist = p->yhist;
+    T.yh = p->yh;
+    T.outs = outs_dev;
+    T.loss_part = p->loss_part;
+    T.t0 = p->t_next;
+    T.n = int(n);
+    T.part = p->t_part;
+    T.delta = p->t_delta;
+    T.max_n = p->t_maxn;
+    T.gbar = p->t_bars;
+    T.wbar = p->t_bars + 16;
+    T.status = p->d_status;
+    T.timeout_ns = p->timeout_ns;
+    CUDA_TRY(cudaMemsetAsync(p->t_bars, 0, 32 * sizeof(u64), p->stream));
+    void* targs[] = {&T};
+    CUDA_TRY(cudaEventRecord(p->ev0, p->stream));
+    CUDA_TRY(cudaLaunchCooperativeKernel((const void*)pt::tile_kernel, dim3(p->G), dim3(pt::T_THREADS), targs,
+                                         size_t(p->t_smem), p->stream));
+    CUDA_TRY(cudaEventRecord(p->ev1, p->stream));
+  } else {
+    void* args[] = {&P};
+    CUDA_TRY(cudaEventRecord(p->ev0, p->stream));
+    const void* fn = p->fast ? (p->qw == 8 ? (const void*)pt::tick_kernel<true, 8> : (const void*)pt::tick_kernel<true, 4>)
+                             : (p->qw == 8 ? (const void*)pt::tick_kernel<false, 8> : (const void*)pt::tick_kernel<false, 4>);
+    CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(p->G), dim3(pt::NTHREADS), args, size_t(p->smem_bytes), p->stream));
+    CUDA_TRY(cudaEventRecord(p->ev1, p->stream));
+  }
   p->timed = true;
 
   if (last) {
@@ -804,6 +943,11 @@ int pt_last_kernel_ms(pt_pipeline* p, float* ms) {
 }
 
 int64_t pt_tick(pt_pipeline* p) { return p ? p->t_next : -1; }
+
+int32_t pt_kernel_path(const pt_pipeline* p) {
+  if (!p) return fail(PT_EINVAL, "null handle");
+  return p->tile ? PT_PATH_TILE : PT_PATH_TICK;
+}
 
 int pt_set_trace(pt_pipeline* p, int32_t cta, int32_t cap) {
   if (!p) return fail(PT_EINVAL, "null handle");

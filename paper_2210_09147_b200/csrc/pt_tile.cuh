@@ -1,0 +1,605 @@
+// pt_tile.cuh: the micro-batch (M >= 16) PARTIME tick kernel on the tcgen05 tensor cores.
+//
+// Same tick contract as pt::tick_kernel (
+// PAPER.md Alg. 1, Eqs. 6-10), different execution: at M = 16 a dense layer is a real
+// contraction (8 flop/B), so each step is a swap-AB GEMM on the tensor core with the
+// weights as the 128-row A operand and the micro-batch as N:
+//   F_i : Z[r][m]  = sum_c W[r][c] a[m][c]   A = W  tile, K-major SWIZZLE_128B (TMA)
+//   B_i : G[c][m]  = sum_r W[r][c] d[m][r]   A = W^T tile, MN-major SWIZZLE_128B_BASE32B
+//                                             (TMA, the same row-major weights, no transpose)
+//         W[r][c] -= lr sum_m d[m][r] a[m][c] fused SIMT epilogue on the same smem tile,
+//                                             written back by TMA store
+// fp32 parity: 3xTF32 (hi*hi + hi*lo + lo*hi). The SIMT warps split every tile into
+// hi = tf32(w) (in place) and lo = w - hi (second buffer); the update rebuilds w = hi + lo
+// exactly before applying the SGD step.
+//
+// Work split (one CTA per SM, G <= 148, cooperative launch):
+//   F step of a layer [n_out x n_in]: units (128-row block, column quarter); CTA c takes
+//   units c, c+G, ...; a unit streams 64-column chunks (two 32 KB TMA boxes).
+//   B step: units (128-column block, row quarter), 64-row chunks (four 8 KB boxes).
+//   Each unit leaves a partial (over its quarter) in TMEM; the 4 partials are summed in a
+//   fixed order by a distributed finalize after a grid barrier (bias, activation, loss,
+//   delta, stage exchange), then a second grid barrier publishes the result. All
+//   reductions are fixed-order: runs are bitwise reproducible.
+// Warp roles: warp 0 = TMA producer (runs ahead across steps and ticks, stores updated
+// tiles back), warp 1 = MMA issuer (one thread), warps 2..9 = SIMT (split, operand
+// staging, TMEM epilogue, update, finalize, grid barrier).
+// Single process, every stage on this GPU (the multi-GPU path is pt::tick_kernel).
+#pragma once
+#include "pt_kernels.cuh"
+#include "pt_tc.cuh"
+
+namespace pt {
+
+constexpr int T_THREADS = 320;
+constexpr int T_SIMT0 = 64;            // first SIMT thread
+constexpr int T_NS = 256;              // SIMT threads
+constexpr int T_NSLOT = 4;             // weight ring slots of 32 KB
+constexpr int T_SLOT_FLOATS = 8192;
+constexpr int T_CK = 64;               // F: chunk columns; B: chunk rows
+constexpr int T_Q = 4;                 // quarters (columns in F, rows in B)
+constexpr int T_MAXM = 16;
+
+struct TLayer {
+  const CUtensorMap* tmf;  // box [128 rows][32 cols], SWIZZLE_128B
+  const CUtensorMap* tmb;  // box [64 rows][32 cols], SWIZZLE_128B_ATOM_32B
+  float* b;
+  int n_in, n_out, act;
+  int a_in, a_out;  // offsets (floats) of a_i, a_{i+1} in a stage cache slot ([M][n] each)
+};
+
+struct TStage {
+  int h, first, k, n0, nk;
+  float* cache[2];       // a_0 (private copy of the stage input) .. a_k, per tick parity
+  float* inslot[2];      // [M][n0], written by the upstream stage
+  float* gslot[2];       // [M][nk], written by the downstream stage
+  float* down_inslot[2]; // downstream stage's inslot (h < D)
+  float* up_gslot[2];    // upstream stage's gslot (h > 1)
+};
+
+struct TParams {
+  const TStage* stages;
+  const TLayer* layers;
+  int n_stages, M, D, learn, act_delay, F, G;
+  float lr;
+  const float* xs;  // [n][M][ldx]
+  int ldx;
+  const float* ys;  // [n][M][F]
+  const float* yhist;
+  int yh;
+  float* outs;       // [n][M][F]
+  float* loss_part;  // [n][G]
+  long long t0;
+  int n;
+  float* part;   // [T_Q][M][max_n] unit partials
+  float* delta;  // [M][max_n] delta of the current B layer
+  int max_n;
+  u64* gbar;     // grid barrier counter (monotonic)
+  u64* wbar;     // per-tick "weights written back" counter (monotonic)
+  u64 gbar_base, wbar_base;
+  int* status;
+  unsigned long long timeout_ns;
+};
+
+// ------------------------------------------------------------------ schedule
+// The producer, the MMA issuer and the SIMT warps walk the same sequence of
+// (tick, stage, step, unit, chunk); chunk j uses ring slot j % T_NSLOT and operand /
+// lo buffer j % 2.
+struct TStep {
+  int L;        // layer index
+  bool fwd;
+  int nunits, nchunks;
+};
+__device__ __forceinline__ TStep t_step(const TParams& P, const TStage& S, int st) {
+  TStep s;
+  s.fwd = st < S.k;
+  const int i = s.fwd ? st : 2 * S.k - 1 - st;
+  s.L = S.first + i;
+  const TLayer& L = P.layers[s.L];
+  if (s.fwd) {
+    s.nunits = (L.n_out / 128) * T_Q;
+    s.nchunks = L.n_in / T_Q / T_CK;
+  } else {
+    s.nunits = (L.n_in / 128) * T_Q;
+    s.nchunks = L.n_out / T_Q / T_CK;
+  }
+  return s;
+}
+__device__ __forceinline__ int t_nsteps(const TParams& P, const TStage& S) { return P.learn ? 2 * S.k : S.k; }
+__device__ __forceinline__ bool t_upd(const TParams& P, long long t, int h) {
+  return P.learn && P.lr != 0.f && t >= 2LL * P.D - h - 1;  // warm-up gate SPEC.md:254
+}
+
+// --------------------------------------------------------------- small helpers
+__device__ __forceinline__ bool t_watch(const TParams& P, uint64_t t_start) {
+  if (ld_volatile_s32(P.status) != ST_OK) return true;
+  if (globaltimer() - t_start > P.timeout_ns) {
+    atomicCAS(P.status, ST_OK, ST_TIMEOUT);
+    return true;
+  }
+  return false;
+}
+__device__ __forceinline__ void t_wait(uint64_t* bar, uint32_t parity, const TParams& P) {
+  if (mbar_try_wait(bar, parity)) return;
+  const uint64_t t0 = globaltimer();
+  while (!mbar_try_wait(bar, parity))
+    if (t_watch(P, t0)) return;
+}
+__device__ __forceinline__ void simt_sync() { asm volatile("bar.sync 1, %0;" ::"n"(T_NS) : "memory"); }
+__device__ __forceinline__ float t_ld(const float* p) { return __ldcg(p); }
+__device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+
+// grid barrier among the SIMT groups of all CTAs (counter never reset: target = G * k)
+__device__ void t_grid_sync(const TParams& P, u64& gen) {
+  simt_sync();
+  ++gen;
+  if (threadIdx.x == T_SIMT0) {
+    red_release_gpu(P.gbar, 1);
+    const u64 target = P.gbar_base + u64(P.G) * gen;
+    if (ld_acquire_gpu(P.gbar) < target) {
+      const uint64_t t0 = globaltimer();
+      for (unsigned it = 1;; ++it) {
+        if (ld_acquire_gpu(P.gbar) >= target) break;
+        if ((it & 63u) == 0 && t_watch(P, t0)) break;
+      }
+    }
+  }
+  simt_sync();
+}
+
+struct TSmem {
+  float* ring;      // T_NSLOT x 32 KB (1024-B aligned)
+  float* lo;        // 2 x 32 KB
+  float* opnd;      // 2 x (hi, lo) x [M][64] no-swizzle K-major
+  float* dT;        // B: delta of the chunk rows, [64][M] (row-major by r)
+  float* red;       // 16 floats
+  uint64_t* full;   // [T_NSLOT]
+  uint64_t* sfree;  // [T_NSLOT] slot consumed (F: MMAs done; B: update done)
+  uint64_t* prep;   // [2]
+  uint64_t* mdone;  // [2]
+  uint64_t* afree;  // [2] accumulator read by the epilogue
+  uint32_t* tmem;
+};
+
+// ------------------------------------------------------------------ producer
+__device__ void t_producer(const TParams& P, const TSmem& sm) {
+  const int c = blockIdx.x, G = P.G;
+  uint32_t j = 0;
+  // pending write-backs: slot -> (layer, row, col) of the tile, valid flag
+  int pend_l[T_NSLOT], pend_r[T_NSLOT], pend_c[T_NSLOT];
+  uint32_t pend_j[T_NSLOT];
+  bool pend[T_NSLOT];
+  for (int s = 0; s < T_NSLOT; ++s) pend[s] = false;
+  bool dead = false;
+  auto flush = [&](int s) {
+    if (!pend[s]) return;
+    t_wait(&sm.sfree[s], (pend_j[s] / T_NSLOT) & 1, P);
+    const CUtensorMap* tm = P.layers[pend_l[s]].tmb;
+    float* base = sm.ring + size_t(s) * T_SLOT_FLOATS;
+    for (int b = 0; b < 4; ++b) tma_store_2d(tm, base + b * 2048, pend_c[s] + 32 * b, pend_r[s]);
+    pend[s] = false;
+  };
+  for (int ti = 0; ti < P.n && !dead; ++ti) {
+    const long long t = P.t0 + ti;
+    if (P.learn && ti > 0) {
+      // weights of tick t-1 are written back by every CTA before any tile of tick t is read
+      const u64 target = P.wbar_base + u64(G) * u64(ti);
+      const uint64_t t0 = globaltimer();
+      while (ld_acquire_gpu(P.wbar) < target)
+        if (t_watch(P, t0)) {
+          dead = true;
+          break;
+        }
+      fence_proxy_async_global();
+    }
+    for (int s = 0; s < P.n_stages && !dead; ++s) {
+      const TStage& S = P.stages[s];
+      const bool upd = t_upd(P, t, S.h);
+      for (int st = 0; st < t_nsteps(P, S); ++st) {
+        const TStep sp = t_step(P, S, st);
+        const TLayer& L = P.layers[sp.L];
+        for (int u = c; u < sp.nunits; u += G) {
+          const int blk = u / T_Q, q = u % T_Q;
+          for (int ch = 0; ch < sp.nchunks; ++ch, ++j) {
+            const int slot = j % T_NSLOT;
+            if (j >= T_NSLOT) {
+              if (pend[slot]) {
+                flush(slot);
+                bulk_commit();
+                bulk_wait_read_all();
+              } else {
+                t_wait(&sm.sfree[slot], ((j - T_NSLOT) / T_NSLOT) & 1, P);
+              }
+            }
+            float* dst = sm.ring + size_t(slot) * T_SLOT_FLOATS;
+            mbar_arrive_expect_tx(&sm.full[slot], T_SLOT_FLOATS * 4);
+            if (sp.fwd) {
+              const int r0 = blk * 128, c0 = q * (L.n_in / T_Q) + ch * T_CK;
+              tma_load_2d(dst, L.tmf, c0, r0, &sm.full[slot]);
+              tma_load_2d(dst + 4096, L.tmf, c0 + 32, r0, &sm.full[slot]);
+            } else {
+              const int c0 = blk * 128, r0 = q * (L.n_out / T_Q) + ch * T_CK;
+              for (int b = 0; b < 4; ++b) tma_load_2d(dst + b * 2048, L.tmb, c0 + 32 * b, r0, &sm.full[slot]);
+              if (upd) {
+                pend[slot] = true;
+                pend_l[slot] = sp.L;
+                pend_r[slot] = r0;
+                pend_c[slot] = c0;
+                pend_j[slot] = j;
+              }
+            }
+            if (ld_volatile_s32(P.status) != ST_OK) dead = true;
+          }
+        }
+      }
+    }
+    if (P.learn) {
+      // end of tick: write back every updated tile still in the ring, then publish
+      for (uint32_t k = 0; k < T_NSLOT; ++k) flush(int((j + k) % T_NSLOT));
+      bulk_commit();
+      bulk_wait_all();
+      fence_proxy_async_global();
+      red_release_gpu(P.wbar, 1);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ MMA issuer
+__device__ void t_mma(const TParams& P, const TSmem& sm, uint32_t tbase) {
+  const int c = blockIdx.x, G = P.G, M = P.M;
+  const uint32_t idf = tc_idesc_tf32(128, M, false, false);
+  const uint32_t idb = tc_idesc_tf32(128, M, true, false);
+  uint32_t j = 0, uc = 0;  // chunk, unit counters
+  const int ob = M * T_CK;  // floats of one operand half
+  for (int ti = 0; ti < P.n; ++ti) {
+    for (int s = 0; s < P.n_stages; ++s) {
+      const TStage& S = P.stages[s];
+      for (int st = 0; st < t_nsteps(P, S); ++st) {
+        const TStep sp = t_step(P, S, st);
+        for (int u = c; u < sp.nunits; u += G, ++uc) {
+          const uint32_t acc = tbase + (uc & 1) * uint32_t(M);
+          if (uc >= 2) t_wait(&sm.afree[uc & 1], ((uc - 2) >> 1) & 1, P);
+          for (int ch = 0; ch < sp.nchunks; ++ch, ++j) {
+            const int slot = j % T_NSLOT, b = j & 1;
+            t_wait(&sm.prep[b], (j >> 1) & 1, P);
+            tc_fence_after();
+            const float* hi = sm.ring + size_t(slot) * T_SLOT_FLOATS;
+            const float* lo = sm.lo + size_t(b) * T_SLOT_FLOATS;
+            const float* ohi = sm.opnd + size_t(b) * 2 * ob;
+            const float* olo = ohi + ob;
+            for (int ks = 0; ks < T_CK / 8; ++ks) {
+              uint64_t dh, dl;
+              if (sp.fwd) {
+                dh = tc_desc_kmajor_sw128(hi + (ks >> 2) * 4096, (ks & 3) * 32);
+                dl = tc_desc_kmajor_sw128(lo + (ks >> 2) * 4096, (ks & 3) * 32);
+              } else {
+                dh = tc_desc_mn_sw128b32(hi, ks * 8, 8192);
+                dl = tc_desc_mn_sw128b32(lo, ks * 8, 8192);
+              }
+              const uint64_t bh = tc_desc_kmajor_noswz(ohi, ks, T_CK), bl = tc_desc_kmajor_noswz(olo, ks, T_CK);
+              const uint32_t id = sp.fwd ? idf : idb;
+              tc_mma_tf32(acc, dh, bh, id, ch > 0 || ks > 0);
+              tc_mma_tf32(acc, dh, bl, id, true);
+              tc_mma_tf32(acc, dl, bh, id, true);
+            }
+            tc_commit(&sm.mdone[b]);
+            if (sp.fwd) tc_commit(&sm.sfree[slot]);
+          }
+        }
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ SIMT side
+// stage an [M][64] fp32 operand chunk (rows m, 64 consecutive k) as tf32 hi / lo in the
+// no-swizzle K-major layout
+__device__ __forceinline__ void t_stage_opnd(float* ohi, float* olo, const float* src, int ld, int M) {
+  const int tid = threadIdx.x - T_SIMT0;
+  for (int i = tid; i < M * 16; i += T_NS) {
+    const int m = i >> 4, k = (i & 15) * 4;
+    const float4 v = ldcg4(reinterpret_cast<const float4*>(src + size_t(m) * ld + k));
+    const float x[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const uint32_t off = tc_kmajor_noswz_off(m, k + e, T_CK) >> 2;
+      const float h = tf32_hi(x[e]);
+      ohi[off] = h;
+      olo[off] = x[e] - h;
+    }
+  }
+}
+
+// split a ring tile in place into tf32 hi, and lo = w - hi into the lo buffer
+__device__ __forceinline__ void t_split(float* tile, float* lo) {
+  const int tid = threadIdx.x - T_SIMT0;
+  float4* t4 = reinterpret_cast<float4*>(tile);
+  float4* l4 = reinterpret_cast<float4*>(lo);
+#pragma unroll 4
+  for (int i = tid; i < T_SLOT_FLOATS / 4; i += T_NS) {
+    const float4 w = t4[i];
+    float4 h, l;
+    h.x = tf32_hi(w.x); l.x = w.x - h.x;
+    h.y = tf32_hi(w.y); l.y = w.y - h.y;
+    h.z = tf32_hi(w.z); l.z = w.z - h.z;
+    h.w = tf32_hi(w.w); l.w = w.w - h.w;
+    t4[i] = h;
+    l4[i] = l;
+  }
+}
+
+// B-chunk update on the ATOM_32B tile [64 rows][4 boxes x 32 cols]:
+// w = hi + lo;  w -= lr * sum_m dT[r][m] * a[m][c]. Thread: one logical column, 32 rows.
+__device__ __forceinline__ void t_update(float* tile, const float* lo, const float* dT, const float (&areg)[T_MAXM],
+                                         int M, float nlr) {
+  const int tid = threadIdx.x - T_SIMT0;
+  const int cl = tid & 127, rh = tid >> 7;  // logical column in the chunk, row half
+  const int box = cl >> 5, g = (cl >> 3) & 3, e = cl & 7;
+  for (int rr = 0; rr < 32; ++rr) {
+    const int r = rh * 32 + rr;
+    const int off = box * 2048 + r * 32 + ((g ^ (r & 3)) << 3) + e;
+    float s = 0.f;
+    const float* d = dT + r * M;
+#pragma unroll
+    for (int m = 0; m < T_MAXM; ++m)
+      if (m < M) s = fmaf(d[m], areg[m], s);
+    const float w = tile[off] + lo[off];
+    tile[off] = fmaf(nlr, s, w);
+  }
+}
+
+__global__ void __launch_bounds__(T_THREADS, 1) tile_kernel(const __grid_constant__ TParams P) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // 1024-B alignment of the swizzled tiles
+  unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  TSmem sm;
+  const int M = P.M, G = P.G, c = blockIdx.x;
+  const int ob = M * T_CK;
+  sm.ring = reinterpret_cast<float*>(base);
+  sm.lo = sm.ring + T_NSLOT * T_SLOT_FLOATS;
+  sm.opnd = sm.lo + 2 * T_SLOT_FLOATS;
+  sm.dT = sm.opnd + 2 * 2 * ob;
+  sm.red = sm.dT + T_CK * M;
+  sm.full = reinterpret_cast<uint64_t*>(sm.red + 16);
+  sm.sfree = sm.full + T_NSLOT;
+  sm.prep = sm.sfree + T_NSLOT;
+  sm.mdone = sm.prep + 2;
+  sm.afree = sm.mdone + 2;
+  sm.tmem = reinterpret_cast<uint32_t*>(sm.afree + 2);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < T_NSLOT; ++s) {
+      mbar_init(&sm.full[s], 1);
+      mbar_init(&sm.sfree[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&sm.prep[b], 1);
+      mbar_init(&sm.mdone[b], 1);
+      mbar_init(&sm.afree[b], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(sm.tmem, 2 * M < 32 ? 32 : 2 * M);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *sm.tmem;
+
+  if (warp == 0) {
+    if (lane == 0) t_producer(P, sm);
+  } else if (warp == 1) {
+    if (lane == 0) t_mma(P, sm, tbase);
+  } else {
+    // ================================================================ SIMT
+    const int st_id = tid - T_SIMT0;           // 0..255
+    const int gtid = c * T_NS + st_id, gthreads = G * T_NS;
+    const float nlr = -P.lr;
+    const float inv_mf = 1.f / float(M * P.F);
+    uint32_t j = 0, uc = 0;
+    u64 gen = 0;
+    for (int ti = 0; ti < P.n; ++ti) {
+      const long long t = P.t0 + ti;
+      const int cur = int(t & 1), prv = cur ^ 1;
+      for (int s = 0; s < P.n_stages; ++s) {
+        const TStage& S = P.stages[s];
+        const int h = S.h;
+        const bool is_last = (h == P.D);
+        const bool upd = t_upd(P, t, h);
+        float* Ccur = S.cache[cur];
+        const float* Cb = (h < P.D && P.act_delay) ? S.cache[prv] : S.cache[cur];  // backward cache
+        // stage input: x_t (h = 1) or inslot[(t-1) % 2]
+        const float* in;
+        int ld_in0;
+        if (h == 1) {
+          in = P.xs + size_t(ti) * M * P.ldx;
+          ld_in0 = P.ldx;
+        } else {
+          in = S.inslot[prv];
+          ld_in0 = S.n0;
+        }
+        // private copy of the stage input (inslot is overwritten at t+1 before B reads it)
+        for (int e = gtid; e < M * S.n0; e += gthreads) {
+          const int m = e / S.n0, k = e - m * S.n0;
+          Ccur[size_t(m) * S.n0 + k] = t_ld(in + size_t(m) * ld_in0 + k);
+        }
+        for (int st = 0; st < t_nsteps(P, S); ++st) {
+          const TStep sp = t_step(P, S, st);
+          const TLayer& L = P.layers[sp.L];
+          const int i = sp.L - S.first;
+          // ---------------------------------------------------- compute
+          if (!sp.fwd && upd && c < T_Q) {
+            // bias of this layer: rows of quarter c, b -= lr * sum_m delta
+            const int rq = L.n_out / T_Q;
+            for (int r = c * rq + st_id; r < (c + 1) * rq; r += T_NS) {
+              float sd = 0.f;
+              for (int m = 0; m < M; ++m) sd += t_ld(P.delta + size_t(m) * P.max_n + r);
+              L.b[r] = fmaf(nlr, sd, t_ld(L.b + r));
+            }
+          }
+          for (int u = c; u < sp.nunits; u += G, ++uc) {
+            const int blk = u / T_Q, q = u % T_Q;
+            float areg[T_MAXM];
+            if (!sp.fwd && upd) {
+              // a_i[m][col] of this thread's update column, from the backward cache
+              const int col = blk * 128 + (st_id & 127);
+#pragma unroll
+              for (int m = 0; m < T_MAXM; ++m)
+                areg[m] = m < M ? t_ld(Cb + L.a_in + size_t(m) * L.n_in + col) : 0.f;
+            }
+            const uint32_t j0 = j;
+            for (int ch = 0; ch < sp.nchunks; ++ch, ++j) {
+              const int slot = j % T_NSLOT, b = j & 1;
+              float* tile = sm.ring + size_t(slot) * T_SLOT_FLOATS;
+              float* lo = sm.lo + size_t(b) * T_SLOT_FLOATS;
+              float* ohi = sm.opnd + size_t(b) * 2 * ob;
+              if (j >= 2) t_wait(&sm.mdone[b], ((j - 2) >> 1) & 1, P);  // lo/operand buffer free
+              // operand chunk: F = a_i[:, cols], B = delta[:, rows]
+              if (sp.fwd) {
+                const int c0 = q * (L.n_in / T_Q) + ch * T_CK;
+                const float* src = (i == 0) ? in + c0 : Ccur + L.a_in + c0;
+                t_stage_opnd(ohi, ohi + ob, src, i == 0 ? ld_in0 : L.n_in, M);
+              } else {
+                const int r0 = q * (L.n_out / T_Q) + ch * T_CK;
+                t_stage_opnd(ohi, ohi + ob, P.delta + r0, P.max_n, M);
+              }
+              t_wait(&sm.full[slot], (j / T_NSLOT) & 1, P);
+              t_split(tile, lo);
+              fence_proxy_async_shared();
+              simt_sync();
+              if (st_id == 0) mbar_arrive(&sm.prep[b]);
+              if (!sp.fwd) {
+                // update of the previous chunk once its MMAs (which read the pre-update
+                // tile) are done; the producer then stores it back
+                if (ch > 0) {
+                  const uint32_t jp = j - 1;
+                  const int sp_slot = jp % T_NSLOT, bp = jp & 1;
+                  t_wait(&sm.mdone[bp], (jp >> 1) & 1, P);
+                  if (upd) {
+                    float* tp = sm.ring + size_t(sp_slot) * T_SLOT_FLOATS;
+                    // dT for the previous chunk's rows
+                    const int r0p = q * (L.n_out / T_Q) + (ch - 1) * T_CK;
+                    for (int e = st_id; e < T_CK * M; e += T_NS) {
+                      const int r = e / M, m = e - r * M;
+                      sm.dT[e] = t_ld(P.delta + size_t(m) * P.max_n + r0p + r);
+                    }
+                    simt_sync();
+                    t_update(tp, sm.lo + size_t(bp) * T_SLOT_FLOATS, sm.dT, areg, M, nlr);
+                    fence_proxy_async_shared();
+                    simt_sync();
+                  }
+                  if (st_id == 0) mbar_arrive(&sm.sfree[sp_slot]);
+                }
+              }
+            }
+            // unit epilogue: last chunk's MMAs complete -> accumulator
+            const uint32_t jl = j - 1;
+            t_wait(&sm.mdone[jl & 1], (jl >> 1) & 1, P);
+            tc_fence_after();
+            if (!sp.fwd) {
+              const int slot = jl % T_NSLOT, bl = jl & 1;
+              if (upd) {
+                const int r0p = q * (L.n_out / T_Q) + (sp.nchunks - 1) * T_CK;
+                for (int e = st_id; e < T_CK * M; e += T_NS) {
+                  const int r = e / M, m = e - r * M;
+                  sm.dT[e] = t_ld(P.delta + size_t(m) * P.max_n + r0p + r);
+                }
+                simt_sync();
+                t_update(sm.ring + size_t(slot) * T_SLOT_FLOATS, sm.lo + size_t(bl) * T_SLOT_FLOATS, sm.dT, areg, M,
+                         nlr);
+                fence_proxy_async_shared();
+                simt_sync();
+              }
+              if (st_id == 0) mbar_arrive(&sm.sfree[slot]);
+            }
+            (void)j0;
+            // TMEM -> partials: warps 2..5 cover lane quarters 2,3,0,1
+            if (warp < 6) {
+              const int lq = warp & 3;
+              const uint32_t ta = tbase + (uc & 1) * uint32_t(M) + ((uint32_t(lq) * 32) << 16);
+              float v[16], v2[16];
+              tmem_ld_32x32b_x16(ta, v);
+              if (M > 16) tmem_ld_32x32b_x16(ta + 16, v2);
+              const int rowcol = blk * 128 + lq * 32 + lane;  // F: output row; B: input column
+              float* dst = P.part + size_t(q) * M * P.max_n + rowcol;
+              for (int m = 0; m < M && m < 16; ++m) dst[size_t(m) * P.max_n] = v[m];
+              for (int m = 16; m < M; ++m) dst[size_t(m) * P.max_n] = v2[m - 16];
+            }
+            tc_fence_before();
+            simt_sync();
+            if (st_id == 0) mbar_arrive(&sm.afree[uc & 1]);
+          }
+          t_grid_sync(P, gen);
+          // ---------------------------------------------------- finalize
+          if (sp.fwd) {
+            const bool last_layer = (i == S.k - 1);
+            const bool last_of_net = last_layer && is_last;
+            const long long sid = t - (P.D - 1);
+            const float* y = nullptr;
+            if (last_of_net && sid >= 0) {
+              if (sid >= P.t0) y = P.ys ? P.ys + size_t(sid - P.t0) * M * P.F : nullptr;
+              else if (P.yhist) y = P.yhist + size_t(sid % P.yh) * M * P.F;
+            }
+            float lacc = 0.f;
+            const int n = L.n_out;
+            for (int e = gtid; e < M * n; e += gthreads) {
+              const int m = e / n, r = e - m * n;
+              float z = 0.f;
+#pragma unroll
+              for (int qq = 0; qq < T_Q; ++qq) z += t_ld(P.part + (size_t(qq) * M + m) * P.max_n + r);
+              z += t_ld(L.b + r);
+              const float a = act_fn(L.act, z);
+              Ccur[L.a_out + size_t(m) * n + r] = a;
+              if (last_layer && h < P.D) S.down_inslot[cur][size_t(m) * n + r] = a;
+              if (last_of_net) {
+                P.outs[(size_t(ti) * M + m) * P.F + r] = a;
+                float g = 0.f;
+                if (y) {
+                  const float d = a - y[size_t(m) * P.F + r];
+                  lacc = fmaf(d, d, lacc);
+                  g = 2.f * d * inv_mf;
+                }
+                if (P.learn) P.delta[size_t(m) * P.max_n + r] = g * dact_fn(L.act, a);
+              } else if (last_layer && P.learn) {
+                // delta of the stage's last layer from the downstream gradient sent at t-1
+                const float ao = (P.act_delay) ? t_ld(Cb + L.a_out + size_t(m) * n + r) : a;
+                P.delta[size_t(m) * P.max_n + r] = t_ld(S.gslot[prv] + size_t(m) * n + r) * dact_fn(L.act, ao);
+              }
+            }
+            if (last_of_net) {
+              // fixed-order CTA sum of the loss partials
+              float v = warp_sum(lacc);
+              if (lane == 0) sm.red[warp - 2] = v;
+              simt_sync();
+              if (st_id == 0) {
+                float sacc = 0.f;
+                for (int w = 0; w < T_NS / 32; ++w) sacc += sm.red[w];
+                P.loss_part[size_t(ti) * G + c] = sacc;
+              }
+            }
+          } else {
+            const int n = L.n_in;
+            for (int e = gtid; e < M * n; e += gthreads) {
+              const int m = e / n, col = e - m * n;
+              float g = 0.f;
+#pragma unroll
+              for (int qq = 0; qq < T_Q; ++qq) g += t_ld(P.part + (size_t(qq) * M + m) * P.max_n + col);
+              if (i > 0) {
+                const float ai = t_ld(Cb + L.a_in + size_t(m) * n + col);
+                const TLayer& Lp = P.layers[sp.L - 1];
+                P.delta[size_t(m) * P.max_n + col] = g * dact_fn(Lp.act, ai);
+              } else if (h > 1) {
+                S.up_gslot[cur][size_t(m) * n + col] = g;
+              }
+            }
+          }
+          t_grid_sync(P, gen);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_free(tbase, 2 * M < 32 ? 32 : 2 * M);
+}
+
+}  // namespace pt

@@ -254,6 +254,14 @@ class Pipeline:
         raw = getattr(stream, "cuda_stream", stream)
         _lib.check(self._lib.pt_set_stream(self._h, ctypes.c_void_p(raw) if raw else None), "set_stream")
 
+    @property
+    def kernel_path(self):
+        """'tile' (tcgen05 tensor-core tile kernel, batch 16) or 'tick' (per-row SIMT kernel)."""
+        r = self._lib.pt_kernel_path(self._h)
+        if r < 0:
+            _lib.check(r, "kernel_path")
+        return "tile" if r == 1 else "tick"
+
     def last_kernel_ms(self):
         ms = ctypes.c_float()
         _lib.check(self._lib.pt_last_kernel_ms(self._h, ctypes.byref(ms)), "last_kernel_ms")

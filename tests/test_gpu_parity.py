@@ -212,3 +212,65 @@ def test_paper_pipeline_api():
         assert abs(float(pipe.loss_buffer) - o.loss) <= 1e-4 * max(1.0, o.loss)
     pipe.sync_to_net()
     assert np.allclose(net[0].weight.detach().numpy(), ref.extract_weights()[0][1], rtol=1e-4, atol=1e-6)
+
+
+# ---------------------------------------------------------------- tensor-core tile path
+# batch 16 with every width a multiple of 256 runs pt::tile_kernel (tcgen05, 3xTF32)
+
+def _tile_case(widths, counts, T, lr, **kw):
+    e = _case(widths, counts, T, lr, M=16, **kw)
+    return e
+
+
+def test_tile_path_selected():
+    m, st, mk = _pipe([256, 512, 256], [2, 1], 0.01, M=16)
+    xs, ys = st.block(0, 2)
+    p = mk(xs, ys)
+    assert p.kernel_path == "tile"
+    p.close()
+    m, st, mk = _pipe([64, 256, 128, 32], [2, 3], 0.01, M=16)
+    xs, ys = st.block(0, 2)
+    p = mk(xs, ys)
+    assert p.kernel_path == "tick"
+    p.close()
+
+
+@pytest.mark.parametrize("D", [1, 2])
+def test_tile_small(D):
+    counts = {1: [5], 2: [2, 3]}[D]
+    _tile_case([256, 512, 256, 256], counts, 12, 0.02)
+
+
+@pytest.mark.parametrize("act_delay", [0, 1])
+def test_tile_act_delay_tanh(act_delay):
+    _tile_case([256, 256, 512, 256], [2, 3], 10, 0.02, act="tanh", act_delay=act_delay)
+
+
+def test_tile_inference():
+    _tile_case([512, 1024, 512, 256], [2, 3], 6, 0.0, learn=False)
+
+
+def test_tile_c4_shape():
+    """Config 4 shapes (4096 wide, batch 16): 4 layers, D=1 and D=2, against the f64 oracle."""
+    _tile_case([4096] * 5, [7], 3, 1e-3)
+    _tile_case([4096] * 5, [4, 3], 4, 1e-3)
+
+
+def test_tile_deterministic_and_split():
+    """Fixed reduction orders: identical runs are bitwise equal, also when split over calls."""
+    res = []
+    for split in (False, True):
+        m, st, mk = _pipe([256, 512, 512, 256], [2, 3], 0.02, M=16)
+        xs, ys = st.block(0, 8)
+        xs, ys = xs.astype(np.float32), ys.astype(np.float32)
+        p = mk(xs, ys)
+        if split:
+            parts = [p.run(xs[i:j], ys[i:j]) for i, j in ((0, 3), (3, 8))]
+            outs = np.concatenate([q[0] for q in parts])
+        else:
+            outs = p.run(xs, ys)[0]
+        res.append((outs, [p.get_layer(j) for j in range(p.L)]))
+        p.close()
+    assert np.array_equal(res[0][0], res[1][0])
+    for (Wa, ba), (Wb, bb) in zip(res[0][1], res[1][1]):
+        assert np.array_equal(Wa, Wb) and np.array_equal(ba, bb)

@@ -19,7 +19,7 @@ constexpr int R = 128, C = 128, MB = 16;
 
 __global__ void __launch_bounds__(128, 1) probe(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_mn,
                                                const __grid_constant__ CUtensorMap tm_out, const float* X, const float* Y,
-                                               float* D, float* E, int variant) {
+                                               float* D, float* E, int variant, float* raw) {
   extern __shared__ __align__(1024) unsigned char smraw[];
   unsigned char* sm = smraw;
   float* sWk = reinterpret_cast<float*>(sm);               // 4 boxes x 16 KB (K-major SW128)
@@ -82,6 +82,7 @@ __global__ void __launch_bounds__(128, 1) probe(const __grid_constant__ CUtensor
     for (int j = 0; j < 16; ++j) D[row * 16 + j] = v[j];
     for (int j = 0; j < 16; ++j) E[row * 16 + j] = v[16 + j];
   }
+  for (int i = tid; i < 4 * 4096; i += blockDim.x) raw[i] = sWm[i];
   // (3) negate the MN tile in smem and store it back through the ATOM_32B map
   __syncthreads();
   for (int i = tid; i < 4 * 4096; i += blockDim.x) sWm[i] = -sWm[i];
@@ -122,12 +123,28 @@ int main() {
   }
   const int smem = 147456 + 64;
   cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  probe<<<1, 128, smem>>>(tk, tmn, tout, dX, dY, dD, dE, 0);
+  float* dRaw;
+  cudaMalloc(&dRaw, 4 * 4096 * 4);
+  probe<<<1, 128, smem>>>(tk, tmn, tout, dX, dY, dD, dE, 0, dRaw);
   cudaError_t e = cudaDeviceSynchronize();
   printf("kernel: %s\n", cudaGetErrorString(e));
   cudaMemcpy(D.data(), dD, D.size() * 4, cudaMemcpyDeviceToHost);
   cudaMemcpy(E.data(), dE, E.size() * 4, cudaMemcpyDeviceToHost);
   cudaMemcpy(Wo.data(), dWo, Wo.size() * 4, cudaMemcpyDeviceToHost);
+  std::vector<float> raw(4 * 4096);
+  cudaMemcpy(raw.data(), dRaw, raw.size() * 4, cudaMemcpyDeviceToHost);
+  // ATOM_32B smem pattern: element (r, 32b + 8g + e) at b*4096 + r*32 + 8*(g ^ f(r)) + e
+  for (int hyp = 0; hyp < 3; ++hyp) {
+    int bad = 0;
+    for (int b = 0; b < 4; ++b)
+      for (int r = 0; r < 128; ++r)
+        for (int g = 0; g < 4; ++g)
+          for (int e = 0; e < 8; ++e) {
+            const int f = hyp == 0 ? (r & 3) : hyp == 1 ? ((r >> 1) & 3) : 0;
+            bad += raw[b * 4096 + r * 32 + 8 * (g ^ f) + e] != W[r * C + 32 * b + 8 * g + e];
+          }
+    printf("ATOM_32B layout hypothesis %d (%s): %d mismatches\n", hyp, hyp == 0 ? "g ^ (r & 3)" : hyp == 1 ? "g ^ ((r>>1) & 3)" : "no swizzle", bad);
+  }
   int bad_d = 0, bad_e = 0, bad_w = 0;
   for (int r = 0; r < R; ++r)
     for (int m = 0; m < 16; ++m) {
