@@ -456,8 +456,8 @@ int setup_tile(pt_pipeline* p) {
   CUDA_TRY(cudaMemcpy(p->d_tlayers, tl.data(), tl.size() * sizeof(pt::TLayer), cudaMemcpyHostToDevice));
   CUDA_TRY(cudaMemcpy(p->d_tstages, ts.data(), ts.size() * sizeof(pt::TStage), cudaMemcpyHostToDevice));
   // shared memory: 1 KB alignment slack, ring, lo, operands, delta tile, reductions, barriers
-  p->t_smem = 1024 + (pt::T_NSLOT + 2) * pt::T_SLOT_FLOATS * 4 + 2 * 2 * M * pt::T_CK * 4 + pt::T_CK * M * 4 + 64 +
-              (2 * pt::T_NSLOT + 6) * 8 + 16;
+  p->t_smem = 1024 + pt::T_NSLOT * pt::T_SLOT_FLOATS * 4 + 2 * 2 * M * pt::T_CK * 4 + 2 * pt::T_CK * pt::T_DTS * 4 + 64 +
+              (2 * pt::T_NSLOT + 10) * 8 + 16;
   if (p->t_smem > pt::SMEM_MAX) return fail(PT_EINVAL, "tile path shared-memory plan exceeds 227 KB");
   CUDA_TRY(cudaFuncSetAttribute(pt::tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, p->t_smem));
   return PT_OK;
@@ -771,6 +771,10 @@ int run_impl(pt_pipeline* p, const float* xs, const float* ys, int64_t n, float*
     T.wbar = p->t_bars + 16;
     T.status = p->d_status;
     T.timeout_ns = p->timeout_ns;
+    T.trace = p->d_trace;
+    T.trace_cap = p->trace_cap;
+    T.trace_cta = p->trace_cta;
+    if (p->d_trace) CUDA_TRY(cudaMemsetAsync(p->d_trace, 0, size_t(p->trace_cap) * sizeof(u64), p->stream));
     CUDA_TRY(cudaMemsetAsync(p->t_bars, 0, 32 * sizeof(u64), p->stream));
     void* targs[] = {&T};
     CUDA_TRY(cudaEventRecord(p->ev0, p->stream));

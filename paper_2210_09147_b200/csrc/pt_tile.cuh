@@ -34,11 +34,15 @@ namespace pt {
 constexpr int T_THREADS = 320;
 constexpr int T_SIMT0 = 64;            // first SIMT thread
 constexpr int T_NS = 256;              // SIMT threads
-constexpr int T_NSLOT = 4;             // weight ring slots of 32 KB
+constexpr int T_NSLOT = 6;             // weight ring slots of 32 KB
 constexpr int T_SLOT_FLOATS = 8192;
 constexpr int T_CK = 64;               // F: chunk columns; B: chunk rows
 constexpr int T_Q = 4;                 // quarters (columns in F, rows in B)
 constexpr int T_MAXM = 16;
+constexpr int T_NACC = 4;              // independent accumulators per unit (K-step % T_NACC)
+constexpr int T_ACC_COLS = 2 * T_NACC * 32;  // TMEM columns of the two unit accumulators
+constexpr int T_TMEM_COLS = 512;        // accumulators + two 64-column lo tiles (A operand in TMEM)
+constexpr int T_DTS = 24;              // dT row stride (floats): conflict-free staging, 16-B rows
 
 struct TLayer {
   const CUtensorMap* tmf;  // box [128 rows][32 cols], SWIZZLE_128B
@@ -79,7 +83,21 @@ struct TParams {
   u64 gbar_base, wbar_base;
   int* status;
   unsigned long long timeout_ns;
+  u64* trace;  // diagnostics: (code << 56) | globaltimer of SIMT thread 0 of CTA trace_cta
+  int trace_cap, trace_cta;
 };
+
+// SIMT thread 0 writes [0, cap/2), the MMA thread [cap/2, 3cap/4), the producer [3cap/4, cap)
+__device__ __forceinline__ void t_trace(const TParams& P, int& idx, int code) {
+  if (P.trace == nullptr || blockIdx.x != P.trace_cta) return;
+  const int tid = threadIdx.x;
+  int lo, hi;
+  if (tid == T_SIMT0) { lo = 0; hi = P.trace_cap / 2; }
+  else if (tid == 32) { lo = P.trace_cap / 2; hi = P.trace_cap - P.trace_cap / 4; }
+  else if (tid == 0) { lo = P.trace_cap - P.trace_cap / 4; hi = P.trace_cap; }
+  else return;
+  if (lo + idx < hi) P.trace[lo + idx++] = (u64(code) << 56) | (globaltimer() & 0x00FFFFFFFFFFFFFFull);
+}
 
 // ------------------------------------------------------------------ schedule
 // The producer, the MMA issuer and the SIMT warps walk the same sequence of
@@ -149,14 +167,15 @@ __device__ void t_grid_sync(const TParams& P, u64& gen) {
 
 struct TSmem {
   float* ring;      // T_NSLOT x 32 KB (1024-B aligned)
-  float* lo;        // 2 x 32 KB
   float* opnd;      // 2 x (hi, lo) x [M][64] no-swizzle K-major
-  float* dT;        // B: delta of the chunk rows, [64][M] (row-major by r)
+  float* dT;        // B: delta of the chunk rows, [2][64][M] (row-major by r), per operand buffer
   float* red;       // 16 floats
   uint64_t* full;   // [T_NSLOT]
   uint64_t* sfree;  // [T_NSLOT] slot consumed (F: MMAs done; B: update done)
-  uint64_t* prep;   // [2]
-  uint64_t* mdone;  // [2]
+  uint64_t* opnd_rdy; // [2] operand chunk staged
+  uint64_t* prep;   // [2] lo tile written (and, in B, the updated weights computed)
+  uint64_t* mhi;    // [2] hi MMAs of the chunk done (raw tile no longer read)
+  uint64_t* mdone;  // [2] all MMAs of the chunk done
   uint64_t* afree;  // [2] accumulator read by the epilogue
   uint32_t* tmem;
 };
@@ -171,6 +190,7 @@ __device__ void t_producer(const TParams& P, const TSmem& sm) {
   bool pend[T_NSLOT];
   for (int s = 0; s < T_NSLOT; ++s) pend[s] = false;
   bool dead = false;
+  int tr = 0;
   auto flush = [&](int s) {
     if (!pend[s]) return;
     t_wait(&sm.sfree[s], (pend_j[s] / T_NSLOT) & 1, P);
@@ -212,6 +232,7 @@ __device__ void t_producer(const TParams& P, const TSmem& sm) {
               }
             }
             float* dst = sm.ring + size_t(slot) * T_SLOT_FLOATS;
+            t_trace(P, tr, 30);
             mbar_arrive_expect_tx(&sm.full[slot], T_SLOT_FLOATS * 4);
             if (sp.fwd) {
               const int r0 = blk * 128, c0 = q * (L.n_in / T_Q) + ch * T_CK;
@@ -246,44 +267,56 @@ __device__ void t_producer(const TParams& P, const TSmem& sm) {
 
 // ------------------------------------------------------------------ MMA issuer
 __device__ void t_mma(const TParams& P, const TSmem& sm, uint32_t tbase) {
+  // Per K-step two MMAs: hi(W) x [a_hi; a_lo] (N = 2M) and lo(W) x a_hi (N = M), both into
+  // the unit accumulator: columns [0, M) collect hi*a_hi + lo*a_hi, [M, 2M) hi*a_lo.
+  // The hi MMAs read the raw TMA tile (the tensor core uses its top 19 bits = tf32(w)),
+  // so they start as soon as the tile lands; the lo MMAs wait for the SIMT split.
   const int c = blockIdx.x, G = P.G, M = P.M;
-  const uint32_t idf = tc_idesc_tf32(128, M, false, false);
-  const uint32_t idb = tc_idesc_tf32(128, M, true, false);
   uint32_t j = 0, uc = 0;  // chunk, unit counters
-  const int ob = M * T_CK;  // floats of one operand half
+  int tr = 0;
   for (int ti = 0; ti < P.n; ++ti) {
     for (int s = 0; s < P.n_stages; ++s) {
       const TStage& S = P.stages[s];
       for (int st = 0; st < t_nsteps(P, S); ++st) {
         const TStep sp = t_step(P, S, st);
+        const uint32_t id2 = tc_idesc_tf32(128, 2 * M, !sp.fwd, false);
+        const uint32_t id1 = tc_idesc_tf32(128, M, false, false);  // A = lo tile in TMEM, K-major
         for (int u = c; u < sp.nunits; u += G, ++uc) {
-          const uint32_t acc = tbase + (uc & 1) * uint32_t(M);
+          // consecutive K-steps go to T_NACC independent accumulators, so back-to-back
+          // small-N MMAs do not wait on each other's accumulation
+          const uint32_t acc = tbase + (uc & 1) * uint32_t(T_NACC * 2 * M);
+          (void)0;
           if (uc >= 2) t_wait(&sm.afree[uc & 1], ((uc - 2) >> 1) & 1, P);
           for (int ch = 0; ch < sp.nchunks; ++ch, ++j) {
             const int slot = j % T_NSLOT, b = j & 1;
-            t_wait(&sm.prep[b], (j >> 1) & 1, P);
-            tc_fence_after();
             const float* hi = sm.ring + size_t(slot) * T_SLOT_FLOATS;
-            const float* lo = sm.lo + size_t(b) * T_SLOT_FLOATS;
-            const float* ohi = sm.opnd + size_t(b) * 2 * ob;
-            const float* olo = ohi + ob;
+            const float* opn = sm.opnd + size_t(b) * 2 * M * T_CK;
+            t_wait(&sm.opnd_rdy[b], (j >> 1) & 1, P);
+            t_wait(&sm.full[slot], (j / T_NSLOT) & 1, P);
+            t_trace(P, tr, 20);
+            tc_fence_after();
+            // descriptors advance by constants per K-step (start-address field, 16-B units):
+            // K-major SW128: +32 B inside the 128-B atom, +16 KB to the next 32-column box;
+            // MN-major SW128_32B: +8 rows = 1 KB; operand (no swizzle): +256 B
+            uint64_t da = sp.fwd ? tc_desc_kmajor_sw128(hi, 0) : tc_desc_mn_sw128b32(hi, 0, 8192);
+            uint64_t db = tc_desc_kmajor_noswz(opn, 0, T_CK);
+#pragma unroll
             for (int ks = 0; ks < T_CK / 8; ++ks) {
-              uint64_t dh, dl;
-              if (sp.fwd) {
-                dh = tc_desc_kmajor_sw128(hi + (ks >> 2) * 4096, (ks & 3) * 32);
-                dl = tc_desc_kmajor_sw128(lo + (ks >> 2) * 4096, (ks & 3) * 32);
-              } else {
-                dh = tc_desc_mn_sw128b32(hi, ks * 8, 8192);
-                dl = tc_desc_mn_sw128b32(lo, ks * 8, 8192);
-              }
-              const uint64_t bh = tc_desc_kmajor_noswz(ohi, ks, T_CK), bl = tc_desc_kmajor_noswz(olo, ks, T_CK);
-              const uint32_t id = sp.fwd ? idf : idb;
-              tc_mma_tf32(acc, dh, bh, id, ch > 0 || ks > 0);
-              tc_mma_tf32(acc, dh, bl, id, true);
-              tc_mma_tf32(acc, dl, bh, id, true);
+              const uint64_t dak = sp.fwd ? da + uint64_t((ks >> 2) * 1024 + (ks & 3) * 2) : da + uint64_t(ks * 64);
+              tc_mma_tf32(acc + (ks % T_NACC) * 2 * M, dak, db + uint64_t(ks * 16), id2, ch > 0 || ks >= T_NACC);
             }
+            tc_commit(&sm.mhi[b]);
+            t_trace(P, tr, 22);
+            t_wait(&sm.prep[b], (j >> 1) & 1, P);
+            t_trace(P, tr, 23);
+            tc_fence_after();
+            const uint32_t lot = tbase + T_ACC_COLS + uint32_t(b) * T_CK;  // lo tile in TMEM
+#pragma unroll
+            for (int ks = 0; ks < T_CK / 8; ++ks)
+              tc_mma_tf32_ts(acc + (ks % T_NACC) * 2 * M, lot + ks * 8, db + uint64_t(ks * 16), id1, true);
             tc_commit(&sm.mdone[b]);
             if (sp.fwd) tc_commit(&sm.sfree[slot]);
+            t_trace(P, tr, 21);
           }
         }
       }
@@ -292,60 +325,99 @@ __device__ void t_mma(const TParams& P, const TSmem& sm, uint32_t tbase) {
 }
 
 // ------------------------------------------------------------------ SIMT side
-// stage an [M][64] fp32 operand chunk (rows m, 64 consecutive k) as tf32 hi / lo in the
-// no-swizzle K-major layout
-__device__ __forceinline__ void t_stage_opnd(float* ohi, float* olo, const float* src, int ld, int M) {
-  const int tid = threadIdx.x - T_SIMT0;
-  for (int i = tid; i < M * 16; i += T_NS) {
-    const int m = i >> 4, k = (i & 15) * 4;
-    const float4 v = ldcg4(reinterpret_cast<const float4*>(src + size_t(m) * ld + k));
-    const float x[4] = {v.x, v.y, v.z, v.w};
+// Operand chunk [M][64] fp32 (rows m, 64 consecutive k), staged as tf32 hi / lo in the
+// no-swizzle K-major layout. Two phases so the L2 loads of chunk j+1 are in flight while
+// chunk j is processed: fetch() issues the loads into registers, put() stores them.
+// With dT != nullptr (B chunks), the exact values are also kept as dT[k][m] for the update.
+struct TOpnd {
+  // thread -> 4 elements (m, k): lane = (m % 8) * 4 + k % 4, so every warp store of the
+  // no-swizzle core-matrix layout hits 32 distinct banks (M == 16: 2 row groups x 16 k-quads)
+  float v[4];
+  __device__ __forceinline__ void fetch(const float* src, int ld, int) {
+    const int st = threadIdx.x - T_SIMT0, lane = st & 31, w = st >> 5;
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const uint32_t off = tc_kmajor_noswz_off(m, k + e, T_CK) >> 2;
-      const float h = tf32_hi(x[e]);
-      ohi[off] = h;
-      olo[off] = x[e] - h;
+    for (int q = 0; q < 4; ++q) {
+      const int idx = w * 4 + q, m = (idx & 1) * 8 + (lane >> 2), k = (idx >> 1) * 4 + (lane & 3);
+      v[q] = __ldcg(src + size_t(m) * ld + k);
     }
   }
-}
-
-// split a ring tile in place into tf32 hi, and lo = w - hi into the lo buffer
-__device__ __forceinline__ void t_split(float* tile, float* lo) {
-  const int tid = threadIdx.x - T_SIMT0;
-  float4* t4 = reinterpret_cast<float4*>(tile);
-  float4* l4 = reinterpret_cast<float4*>(lo);
-#pragma unroll 4
-  for (int i = tid; i < T_SLOT_FLOATS / 4; i += T_NS) {
-    const float4 w = t4[i];
-    float4 h, l;
-    h.x = tf32_hi(w.x); l.x = w.x - h.x;
-    h.y = tf32_hi(w.y); l.y = w.y - h.y;
-    h.z = tf32_hi(w.z); l.z = w.z - h.z;
-    h.w = tf32_hi(w.w); l.w = w.w - h.w;
-    t4[i] = h;
-    l4[i] = l;
-  }
-}
-
-// B-chunk update on the ATOM_32B tile [64 rows][4 boxes x 32 cols]:
-// w = hi + lo;  w -= lr * sum_m dT[r][m] * a[m][c]. Thread: one logical column, 32 rows.
-__device__ __forceinline__ void t_update(float* tile, const float* lo, const float* dT, const float (&areg)[T_MAXM],
-                                         int M, float nlr) {
-  const int tid = threadIdx.x - T_SIMT0;
-  const int cl = tid & 127, rh = tid >> 7;  // logical column in the chunk, row half
-  const int box = cl >> 5, g = (cl >> 3) & 3, e = cl & 7;
-  for (int rr = 0; rr < 32; ++rr) {
-    const int r = rh * 32 + rr;
-    const int off = box * 2048 + r * 32 + ((g ^ (r & 3)) << 3) + e;
-    float s = 0.f;
-    const float* d = dT + r * M;
+  __device__ __forceinline__ void put(float* ohi, float* olo, float* dT, int) const {
+    const int st = threadIdx.x - T_SIMT0, lane = st & 31, w = st >> 5;
 #pragma unroll
-    for (int m = 0; m < T_MAXM; ++m)
-      if (m < M) s = fmaf(d[m], areg[m], s);
-    const float w = tile[off] + lo[off];
-    tile[off] = fmaf(nlr, s, w);
+    for (int q = 0; q < 4; ++q) {
+      const int idx = w * 4 + q, mg = idx & 1, kq = idx >> 1;
+      const int off = mg * 512 + kq * 32 + lane;  // == tc_kmajor_noswz_off(m, k, 64) / 4
+      const float h = tf32_hi(v[q]);
+      ohi[off] = h;
+      olo[off] = v[q] - h;
+      if (dT) dT[(kq * 4 + (lane & 3)) * T_DTS + mg * 8 + (lane >> 2)] = v[q];
+    }
   }
+};
+
+// The lo tile (w - tf32(w)) goes straight from registers to TMEM (tcgen05.st), where the
+// lo MMAs read it as their A operand: lane = M row, column = K element. SIMT warp w owns
+// TMEM lanes 32 * (w % 4) .. +31 and the K half (w - 2) / 4 of the 64-deep chunk.
+//
+// F chunk (K-major SWIZZLE_128B tile, 2 boxes [128 rows][32 cols]): thread = W row r, 32 k.
+__device__ __forceinline__ void t_lo_pass_f(const float* tile, uint32_t lo_tmem) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = 32 * (warp & 3) + lane, kh = (warp - 2) >> 2;
+  const float* row = tile + kh * 4096 + r * 32;
+  float v[32];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const float4 w = *reinterpret_cast<const float4*>(row + ((c ^ (r & 7)) << 2));
+    v[4 * c + 0] = w.x - tf32_hi(w.x);
+    v[4 * c + 1] = w.y - tf32_hi(w.y);
+    v[4 * c + 2] = w.z - tf32_hi(w.z);
+    v[4 * c + 3] = w.w - tf32_hi(w.w);
+  }
+  tmem_st_32x32b_x32(lo_tmem + ((uint32_t(32 * (warp & 3))) << 16) + uint32_t(32 * kh), v);
+  tmem_st_wait();
+}
+
+// B chunk on the ATOM_32B tile [64 rows][4 boxes x 32 cols]: thread = W column c (the A
+// row of W^T), 32 rows. lo^T goes to TMEM; with upd, the SGD step
+// w' = w - lr * sum_m dT[r][m] a[m][c] is kept in registers for t_write_back.
+constexpr int T_UPR = 32;  // rows per thread
+__device__ __forceinline__ int t_bofs(int cl, int r) {
+  const int box = cl >> 5, g = (cl >> 3) & 3, e = cl & 7;
+  return box * 2048 + r * 32 + ((g ^ (r & 3)) << 3) + e;
+}
+__device__ __forceinline__ void t_lo_update_pass(const float* tile, uint32_t lo_tmem, const float* dT,
+                                                 const float (&areg)[T_MAXM], float nlr, bool upd,
+                                                 float (&wn)[T_UPR]) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int cl = 32 * (warp & 3) + lane, rh = (warp - 2) >> 2;
+  float v[32];
+#pragma unroll
+  for (int rr = 0; rr < T_UPR; ++rr) {
+    const int r = rh * T_UPR + rr;
+    const float w = tile[t_bofs(cl, r)];
+    v[rr] = w - tf32_hi(w);
+    if (upd) {
+      const float4* d4 = reinterpret_cast<const float4*>(dT + r * T_DTS);
+      float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+      for (int q = 0; q < T_MAXM / 4; ++q) {
+        const float4 d = d4[q];
+        s0 = fmaf(d.x, areg[4 * q + 0], s0);
+        s1 = fmaf(d.y, areg[4 * q + 1], s1);
+        s0 = fmaf(d.z, areg[4 * q + 2], s0);
+        s1 = fmaf(d.w, areg[4 * q + 3], s1);
+      }
+      wn[rr] = fmaf(nlr, s0 + s1, w);
+    }
+  }
+  tmem_st_32x32b_x32(lo_tmem + ((uint32_t(32 * (warp & 3))) << 16) + uint32_t(32 * rh), v);
+  tmem_st_wait();
+}
+__device__ __forceinline__ void t_write_back(float* tile, const float (&wn)[T_UPR]) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int cl = 32 * (warp & 3) + lane, rh = (warp - 2) >> 2;
+#pragma unroll
+  for (int rr = 0; rr < T_UPR; ++rr) tile[t_bofs(cl, rh * T_UPR + rr)] = wn[rr];
 }
 
 __global__ void __launch_bounds__(T_THREADS, 1) tile_kernel(const __grid_constant__ TParams P) {
@@ -356,14 +428,15 @@ __global__ void __launch_bounds__(T_THREADS, 1) tile_kernel(const __grid_constan
   const int M = P.M, G = P.G, c = blockIdx.x;
   const int ob = M * T_CK;
   sm.ring = reinterpret_cast<float*>(base);
-  sm.lo = sm.ring + T_NSLOT * T_SLOT_FLOATS;
-  sm.opnd = sm.lo + 2 * T_SLOT_FLOATS;
+  sm.opnd = sm.ring + T_NSLOT * T_SLOT_FLOATS;
   sm.dT = sm.opnd + 2 * 2 * ob;
-  sm.red = sm.dT + T_CK * M;
+  sm.red = sm.dT + 2 * T_CK * T_DTS;
   sm.full = reinterpret_cast<uint64_t*>(sm.red + 16);
   sm.sfree = sm.full + T_NSLOT;
-  sm.prep = sm.sfree + T_NSLOT;
-  sm.mdone = sm.prep + 2;
+  sm.opnd_rdy = sm.sfree + T_NSLOT;
+  sm.prep = sm.opnd_rdy + 2;
+  sm.mhi = sm.prep + 2;
+  sm.mdone = sm.mhi + 2;
   sm.afree = sm.mdone + 2;
   sm.tmem = reinterpret_cast<uint32_t*>(sm.afree + 2);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -373,13 +446,15 @@ __global__ void __launch_bounds__(T_THREADS, 1) tile_kernel(const __grid_constan
       mbar_init(&sm.sfree[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
+      mbar_init(&sm.opnd_rdy[b], 1);
+      mbar_init(&sm.mhi[b], 1);
       mbar_init(&sm.prep[b], 1);
       mbar_init(&sm.mdone[b], 1);
       mbar_init(&sm.afree[b], 1);
     }
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc(sm.tmem, 2 * M < 32 ? 32 : 2 * M);
+  if (warp == 1) tmem_alloc(sm.tmem, T_TMEM_COLS);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -397,6 +472,7 @@ __global__ void __launch_bounds__(T_THREADS, 1) tile_kernel(const __grid_constan
     const float inv_mf = 1.f / float(M * P.F);
     uint32_t j = 0, uc = 0;
     u64 gen = 0;
+    int tr = 0;
     for (int ti = 0; ti < P.n; ++ti) {
       const long long t = P.t0 + ti;
       const int cur = int(t & 1), prv = cur ^ 1;
@@ -427,108 +503,119 @@ __global__ void __launch_bounds__(T_THREADS, 1) tile_kernel(const __grid_constan
           const TLayer& L = P.layers[sp.L];
           const int i = sp.L - S.first;
           // ---------------------------------------------------- compute
-          if (!sp.fwd && upd && c < T_Q) {
-            // bias of this layer: rows of quarter c, b -= lr * sum_m delta
-            const int rq = L.n_out / T_Q;
-            for (int r = c * rq + st_id; r < (c + 1) * rq; r += T_NS) {
+          if (!sp.fwd && upd) {
+            // bias of this layer, rows spread over the grid: b -= lr * sum_m delta
+            for (int r = gtid; r < L.n_out; r += gthreads) {
+              float dv[T_MAXM];
+#pragma unroll
+              for (int m = 0; m < T_MAXM; ++m) dv[m] = m < M ? t_ld(P.delta + size_t(m) * P.max_n + r) : 0.f;
               float sd = 0.f;
-              for (int m = 0; m < M; ++m) sd += t_ld(P.delta + size_t(m) * P.max_n + r);
+#pragma unroll
+              for (int m = 0; m < T_MAXM; ++m) sd += dv[m];
               L.b[r] = fmaf(nlr, sd, t_ld(L.b + r));
             }
           }
+          t_trace(P, tr, 1);
           for (int u = c; u < sp.nunits; u += G, ++uc) {
             const int blk = u / T_Q, q = u % T_Q;
             float areg[T_MAXM];
             if (!sp.fwd && upd) {
               // a_i[m][col] of this thread's update column, from the backward cache
-              const int col = blk * 128 + (st_id & 127);
+              const int col = blk * 128 + 32 * (warp & 3) + lane;  // t_lo_update_pass column
 #pragma unroll
               for (int m = 0; m < T_MAXM; ++m)
                 areg[m] = m < M ? t_ld(Cb + L.a_in + size_t(m) * L.n_in + col) : 0.f;
             }
-            const uint32_t j0 = j;
+            // operand source of chunk ch: F = a_i[:, cols], B = delta[:, rows]
+            const float* osrc;
+            int old, ostep;
+            if (sp.fwd) {
+              const int c0 = q * (L.n_in / T_Q);
+              osrc = (i == 0) ? in + c0 : Ccur + L.a_in + c0;
+              old = (i == 0) ? ld_in0 : L.n_in;
+            } else {
+              osrc = P.delta + q * (L.n_out / T_Q);
+              old = P.max_n;
+            }
+            ostep = T_CK;
+            TOpnd op;
+            op.fetch(osrc, old, M);
             for (int ch = 0; ch < sp.nchunks; ++ch, ++j) {
               const int slot = j % T_NSLOT, b = j & 1;
               float* tile = sm.ring + size_t(slot) * T_SLOT_FLOATS;
-              float* lo = sm.lo + size_t(b) * T_SLOT_FLOATS;
+              const uint32_t lot = tbase + T_ACC_COLS + uint32_t(b) * T_CK;  // lo tile in TMEM
               float* ohi = sm.opnd + size_t(b) * 2 * ob;
-              if (j >= 2) t_wait(&sm.mdone[b], ((j - 2) >> 1) & 1, P);  // lo/operand buffer free
-              // operand chunk: F = a_i[:, cols], B = delta[:, rows]
-              if (sp.fwd) {
-                const int c0 = q * (L.n_in / T_Q) + ch * T_CK;
-                const float* src = (i == 0) ? in + c0 : Ccur + L.a_in + c0;
-                t_stage_opnd(ohi, ohi + ob, src, i == 0 ? ld_in0 : L.n_in, M);
-              } else {
-                const int r0 = q * (L.n_out / T_Q) + ch * T_CK;
-                t_stage_opnd(ohi, ohi + ob, P.delta + r0, P.max_n, M);
-              }
-              t_wait(&sm.full[slot], (j / T_NSLOT) & 1, P);
-              t_split(tile, lo);
+              float* dTb = sm.dT + size_t(b) * T_CK * T_DTS;
+              t_trace(P, tr, 6);
+              if (j >= 2) t_wait(&sm.mdone[b], ((j - 2) >> 1) & 1, P);  // operand / lo buffer free
+              tc_fence_after();
+              t_trace(P, tr, 11);
+              op.put(ohi, ohi + ob, sp.fwd ? nullptr : dTb, M);
+              if (ch + 1 < sp.nchunks) op.fetch(osrc + (ch + 1) * ostep, old, M);
               fence_proxy_async_shared();
               simt_sync();
-              if (st_id == 0) mbar_arrive(&sm.prep[b]);
-              if (!sp.fwd) {
-                // update of the previous chunk once its MMAs (which read the pre-update
-                // tile) are done; the producer then stores it back
-                if (ch > 0) {
-                  const uint32_t jp = j - 1;
-                  const int sp_slot = jp % T_NSLOT, bp = jp & 1;
-                  t_wait(&sm.mdone[bp], (jp >> 1) & 1, P);
-                  if (upd) {
-                    float* tp = sm.ring + size_t(sp_slot) * T_SLOT_FLOATS;
-                    // dT for the previous chunk's rows
-                    const int r0p = q * (L.n_out / T_Q) + (ch - 1) * T_CK;
-                    for (int e = st_id; e < T_CK * M; e += T_NS) {
-                      const int r = e / M, m = e - r * M;
-                      sm.dT[e] = t_ld(P.delta + size_t(m) * P.max_n + r0p + r);
-                    }
-                    simt_sync();
-                    t_update(tp, sm.lo + size_t(bp) * T_SLOT_FLOATS, sm.dT, areg, M, nlr);
-                    fence_proxy_async_shared();
-                    simt_sync();
-                  }
-                  if (st_id == 0) mbar_arrive(&sm.sfree[sp_slot]);
+              if (st_id == 0) mbar_arrive(&sm.opnd_rdy[b]);
+              t_trace(P, tr, 12);
+              t_wait(&sm.full[slot], (j / T_NSLOT) & 1, P);
+              t_trace(P, tr, 7);
+              if (sp.fwd) {
+                t_lo_pass_f(tile, lot);
+                t_trace(P, tr, 13);
+                tc_fence_before();
+                simt_sync();
+                if (st_id == 0) mbar_arrive(&sm.prep[b]);
+              } else {
+                float wn[T_UPR];
+                t_lo_update_pass(tile, lot, dTb, areg, nlr, upd, wn);
+                tc_fence_before();
+                simt_sync();
+                if (st_id == 0) mbar_arrive(&sm.prep[b]);
+                t_trace(P, tr, 8);
+                // the hi MMAs read the raw tile: write the update back only after them
+                t_wait(&sm.mhi[b], (j >> 1) & 1, P);
+                t_trace(P, tr, 9);
+                if (upd) {
+                  t_write_back(tile, wn);
+                  fence_proxy_async_shared();
                 }
+                simt_sync();
+                if (st_id == 0) mbar_arrive(&sm.sfree[slot]);
+                t_trace(P, tr, 10);
               }
             }
             // unit epilogue: last chunk's MMAs complete -> accumulator
             const uint32_t jl = j - 1;
             t_wait(&sm.mdone[jl & 1], (jl >> 1) & 1, P);
             tc_fence_after();
-            if (!sp.fwd) {
-              const int slot = jl % T_NSLOT, bl = jl & 1;
-              if (upd) {
-                const int r0p = q * (L.n_out / T_Q) + (sp.nchunks - 1) * T_CK;
-                for (int e = st_id; e < T_CK * M; e += T_NS) {
-                  const int r = e / M, m = e - r * M;
-                  sm.dT[e] = t_ld(P.delta + size_t(m) * P.max_n + r0p + r);
-                }
-                simt_sync();
-                t_update(sm.ring + size_t(slot) * T_SLOT_FLOATS, sm.lo + size_t(bl) * T_SLOT_FLOATS, sm.dT, areg, M,
-                         nlr);
-                fence_proxy_async_shared();
-                simt_sync();
-              }
-              if (st_id == 0) mbar_arrive(&sm.sfree[slot]);
-            }
-            (void)j0;
             // TMEM -> partials: warps 2..5 cover lane quarters 2,3,0,1
             if (warp < 6) {
               const int lq = warp & 3;
-              const uint32_t ta = tbase + (uc & 1) * uint32_t(M) + ((uint32_t(lq) * 32) << 16);
+              const uint32_t ta = tbase + (uc & 1) * uint32_t(T_NACC * 2 * M) + ((uint32_t(lq) * 32) << 16);
               float v[16], v2[16];
               tmem_ld_32x32b_x16(ta, v);
-              if (M > 16) tmem_ld_32x32b_x16(ta + 16, v2);
+              tmem_ld_32x32b_x16(ta + 16, v2);
+#pragma unroll
+              for (int m = 0; m < 16; ++m) v[m] += v2[m];  // (hi + lo) * a_hi + hi * a_lo
+              for (int a = 1; a < T_NACC; ++a) {
+                tmem_ld_32x32b_x16(ta + a * 32, v2);
+#pragma unroll
+                for (int m = 0; m < 16; ++m) v[m] += v2[m];
+                tmem_ld_32x32b_x16(ta + a * 32 + 16, v2);
+#pragma unroll
+                for (int m = 0; m < 16; ++m) v[m] += v2[m];
+              }
               const int rowcol = blk * 128 + lq * 32 + lane;  // F: output row; B: input column
               float* dst = P.part + size_t(q) * M * P.max_n + rowcol;
-              for (int m = 0; m < M && m < 16; ++m) dst[size_t(m) * P.max_n] = v[m];
-              for (int m = 16; m < M; ++m) dst[size_t(m) * P.max_n] = v2[m - 16];
+#pragma unroll
+              for (int m = 0; m < 16; ++m) dst[size_t(m) * P.max_n] = v[m];
             }
             tc_fence_before();
             simt_sync();
             if (st_id == 0) mbar_arrive(&sm.afree[uc & 1]);
           }
+          t_trace(P, tr, 2);
           t_grid_sync(P, gen);
+          t_trace(P, tr, 3);
           // ---------------------------------------------------- finalize
           if (sp.fwd) {
             const bool last_layer = (i == S.k - 1);
@@ -592,14 +679,16 @@ __global__ void __launch_bounds__(T_THREADS, 1) tile_kernel(const __grid_constan
               }
             }
           }
+          t_trace(P, tr, 4);
           t_grid_sync(P, gen);
+          t_trace(P, tr, 5);
         }
       }
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_free(tbase, 2 * M < 32 ? 32 : 2 * M);
+  if (warp == 1) tmem_free(tbase, T_TMEM_COLS);
 }
 
 }  // namespace pt

@@ -1,0 +1,53 @@
+"""Per-phase device timeline of the tcgen05 tile kernel (CTA 0, SIMT thread 0)."""
+import sys, os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+from collections import defaultdict
+from paper_2210_09147_b200 import engine, model as mdl, streams
+
+NAMES = {1: "compute.begin", 2: "compute.end", 3: "barrier1", 4: "finalize", 5: "barrier2", 6: "chunk.begin",
+         7: "full.seen", 11: "mdone.j-2", 12: "opnd.rdy", 13: "lopass.end", 22: "mma.hi.issued", 23: "mma.prep.seen", 8: "prep.done", 9: "mdone.prev", 10: "update.done", 20: "mma.prep", 21: "mma.commit",
+         30: "tma.issue"}
+
+def run(widths, counts, ticks=2, M=16, learn=True, cta=0):
+    m = mdl.mlp(widths, seed=0)
+    st = streams.SmoothStream(widths[0], widths[-1], seed=1, batch=M)
+    xs, ys = st.block(0, ticks)
+    xs = torch.tensor(xs, dtype=torch.float32, device="cuda"); ys = torch.tensor(ys, dtype=torch.float32, device="cuda")
+    p = engine.Pipeline(m, counts, "sgd", 1e-3 if learn else 0.0, xs[0].cpu().numpy(), ys[0].cpu().numpy(), learn=learn)
+    assert p.kernel_path == "tile", p.kernel_path
+    p.run(xs, ys); p.sync()
+    p.set_trace(cta, 1 << 14)
+    p.run(xs, ys); p.sync()
+    ms = p.last_kernel_ms()
+    cons, mma, prod = p.get_trace()
+    L = len(widths) - 1
+    print(f"== {widths[0]}x{L} M={M} learn={learn} counts={counts}: {ms * 1e3 / ticks:.1f} us/tick")
+    dur = defaultdict(list)
+    for (c0, t0), (c1, t1) in zip(cons, cons[1:]):
+        dur[(c0, c1)].append(t1 - t0)
+    for k in sorted(dur, key=lambda k: -sum(dur[k])):
+        v = np.array(dur[k])
+        print(f"  {NAMES.get(k[0], k[0]):>14} -> {NAMES.get(k[1], k[1]):<14} n={len(v):4d} median={np.median(v) / 1e3:8.2f}us "
+              f"total={v.sum() / 1e3 / ticks:9.1f}us/tick")
+    if mma:
+        t = np.array([x for _, x in mma])
+        codes = [c for c, _ in mma]
+        issue = [t[i + 1] - t[i] for i in range(len(t) - 1) if codes[i] == 20 and codes[i + 1] == 21]
+        gap = [t[i + 1] - t[i] for i in range(len(t) - 1) if codes[i] == 21 and codes[i + 1] == 20]
+        print(f"  mma: issue (prep->commit) median {np.median(issue) / 1e3:.2f}us; commit->next prep median {np.median(gap) / 1e3:.2f}us")
+        d = defaultdict(list)
+        for i in range(len(t) - 1):
+            d[(codes[i], codes[i + 1])].append(t[i + 1] - t[i])
+        for k in sorted(d):
+            print(f"    mma {NAMES.get(k[0], k[0])} -> {NAMES.get(k[1], k[1])}: median {np.median(d[k]) / 1e3:.2f}us n={len(d[k])}")
+    if prod:
+        t = np.array([x for _, x in prod])
+        print(f"  producer: {len(t)} loads, median gap {np.median(np.diff(t)) / 1e3:.2f}us")
+    base = cons[0][1]
+    print("  first SIMT events:", [(NAMES.get(c, c), round((x - base) / 1e3, 2)) for c, x in cons[:60]])
+    p.close()
+
+if __name__ == "__main__":
+    run([4096] * 9, [15], ticks=2, learn=False)
+    run([4096] * 9, [15], ticks=2)
