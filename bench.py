@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--layers", type=int, default=LAYERS)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="budget of the cpu_baseline sample")
+    ap.add_argument("--no-extra", action="store_true", help="skip the other BASELINE configs (N=1 only)")
     return ap.parse_args()
 
 
@@ -192,6 +193,59 @@ def run_reference(args):
     }), flush=True)
 
 
+def balanced_counts(widths, D, learn):
+    from paper_2210_09147_b200 import partition
+    L = len(widths) - 1
+    costs, _ = partition.mlp_costs(widths, learn)
+    units, _ = partition.balance(costs, D)
+    out, u = [], 0
+    for c in units:
+        out.append(sum(2 if (u + j) < L - 1 else 1 for j in range(c)))
+        u += c
+    return out
+
+
+def extra_configs(peak):
+    """Device time per tick of the other BASELINE.json configs on this one GPU (all stages
+    here): C3 inference wave, C4 micro-batch 16 (tcgen05 tile kernel), C5 uneven widths.
+    Reported beside the headline line; not part of `value`."""
+    import torch
+    from paper_2210_09147_b200 import engine, model as mdl, streams
+    c5 = [1024, 2048, 4096, 8192, 8192, 4096, 2048, 1024] * 3 + [1024]
+    cases = [("C3", "64-layer 4096-wide MLP inference wave, D=8 stages on 1 GPU", [4096] * 65, 8, False, 1, 8),
+             ("C4", "32-layer 4096-wide MLP, micro-batch 16, D=8 stages on 1 GPU", [4096] * 33, 8, True, 16, 8),
+             ("C5", "uneven widths 1024..8192 (24 layers), D=8 stages on 1 GPU", c5, 8, True, 1, 16)]
+    res = {}
+    for name, desc, widths, D, learn, M, ticks in cases:
+        try:
+            m = mdl.mlp(widths, seed=0, dtype=np.float32)
+            st = streams.SmoothStream(widths[0], widths[-1], seed=1, batch=M)
+            xs, ys = st.block(0, ticks)
+            xs = torch.tensor(xs, dtype=torch.float32, device="cuda")
+            ys = torch.tensor(ys, dtype=torch.float32, device="cuda")
+            x0 = xs[0].cpu().numpy() if M > 1 else xs[0, 0].cpu().numpy()
+            y0 = ys[0].cpu().numpy() if M > 1 else ys[0, 0].cpu().numpy()
+            p = engine.Pipeline(m, balanced_counts(widths, D, learn), "sgd", 1e-3 if learn else 0.0, x0, y0,
+                                learn=learn)
+            best = 1e30
+            for _ in range(3):
+                p.run(xs, ys)
+                p.sync()
+                best = min(best, p.last_kernel_ms())
+            us = best * 1e3 / ticks
+            byt = algorithmic_bytes_per_tick(widths, learn)
+            res[name] = {"workload": desc, "kernel": "pt::tile_kernel (tcgen05)" if p.kernel_path == "tile"
+                         else "pt::tick_kernel", "tick_us": round(us, 1), "samples_per_s": round(M * 1e6 / us, 1),
+                         "achieved_gbs": round(byt / (us * 1e-6) / 1e9, 1),
+                         "frac_of_hbm_roofline": round(byt / (us * 1e-6) / 1e9 / peak, 4)}
+            p.close()
+            del xs, ys
+            torch.cuda.empty_cache()
+        except Exception as e:  # report, do not hide
+            res[name] = {"workload": desc, "error": repr(e)[:200]}
+    return res
+
+
 def load_traffic():
     """dram bytes per tick of the tick kernel from the committed ncu capture, if any."""
     path = os.path.join(ROOT, "profiles", "ncu_tick_kernel.json")
@@ -336,6 +390,9 @@ def main():
     if not args.no_cpu_baseline and world == 1:
         v, cores, sample, _ = cpu_reference(widths, 1, args.cpu_seconds)
         cpu = {"value": round(v, 4), "unit": "samples/s", "cores": cores, "kind": "port", "sample": sample}
+    extra = None
+    if world == 1 and not args.no_extra:
+        extra = extra_configs(peak)
     out = {
         "metric": METRIC, "value": round(value, 2), "unit": "samples/s", "n_gpus": max(world, args.gpus if world == 1 else world),
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 4),
@@ -355,6 +412,7 @@ def main():
                 "d2h_bytes_per_step": d2h},
         "gpu_launches": 2 * args.steps,
         "clocks": clocks,
+        "other_configs": extra,
     }
     print(json.dumps(out), flush=True)
     if world > 1:

@@ -8,6 +8,7 @@
 //   - three activation-cache slots, g_in partial buffers and step counters.
 // All of it is zeroed at create: warm-up ticks read zero slots.
 #include <cuda_runtime.h>
+#include <unistd.h>
 
 #include <atomic>
 #include <cmath>
@@ -78,6 +79,8 @@ struct CommLayout {
 struct IpcBlob {
   int32_t magic, abi, stage, G, M, ld0, ldk, pad_;
   int64_t comm_bytes;
+  int64_t pid;       // exporting process: a same-process import uses dev_ptr directly
+  uint64_t dev_ptr;  // (two handles in one process, e.g. one per GPU or per stream)
   cudaIpcMemHandle_t handle;
 };
 
@@ -993,6 +996,8 @@ int pt_ipc_export(pt_pipeline* p, int32_t stage, void* buf, size_t cap, size_t* 
   b.ld0 = S.ld0;
   b.ldk = S.ldk;
   b.comm_bytes = int64_t(p->layout_of(stage - 1).total);
+  b.pid = int64_t(getpid());
+  b.dev_ptr = uint64_t(reinterpret_cast<uintptr_t>(S.comm));
   CUDA_TRY(cudaIpcGetMemHandle(&b.handle, S.comm));
   memcpy(buf, &b, sizeof(b));
   *len = sizeof(b);
@@ -1014,8 +1019,12 @@ int pt_ipc_import(pt_pipeline* p, const void* buf, size_t len) {
   if (s0 >= lo && s0 < hi) return fail(PT_EINVAL, "stage is local; nothing to import");
   if (s0 != lo - 1 && s0 != hi) return fail(PT_EINVAL, "stage is not a neighbour of the local stages");
   void* ptr = nullptr;
-  CUDA_TRY(cudaIpcOpenMemHandle(&ptr, b.handle, cudaIpcMemLazyEnablePeerAccess));
-  p->ipc_opened.push_back(ptr);
+  if (b.pid == int64_t(getpid())) {
+    ptr = reinterpret_cast<void*>(uintptr_t(b.dev_ptr));  // same process: CUDA IPC cannot reopen it
+  } else {
+    CUDA_TRY(cudaIpcOpenMemHandle(&ptr, b.handle, cudaIpcMemLazyEnablePeerAccess));
+    p->ipc_opened.push_back(ptr);
+  }
   if (s0 == lo - 1) {
     p->stages.front().up = static_cast<char*>(ptr);
     p->stages.front().G_up = b.G;
