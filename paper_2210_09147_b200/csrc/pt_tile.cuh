@@ -34,14 +34,17 @@ namespace pt {
 constexpr int T_THREADS = 320;
 constexpr int T_SIMT0 = 64;            // first SIMT thread
 constexpr int T_NS = 256;              // SIMT threads
-constexpr int T_NSLOT = 6;             // weight ring slots of 32 KB
+constexpr int T_NSLOT = 5;             // weight ring slots of 32 KB
 constexpr int T_SLOT_FLOATS = 8192;
 constexpr int T_CK = 64;               // F: chunk columns; B: chunk rows
 constexpr int T_Q = 4;                 // quarters (columns in F, rows in B)
 constexpr int T_MAXM = 16;
-constexpr int T_NACC = 4;              // independent accumulators per unit (K-step % T_NACC)
+constexpr int T_NACC = 1;              // independent accumulators per unit (K-step % T_NACC)
 constexpr int T_ACC_COLS = 2 * T_NACC * 32;  // TMEM columns of the two unit accumulators
-constexpr int T_TMEM_COLS = 512;        // accumulators + two 64-column lo tiles (A operand in TMEM)
+constexpr int T_TMEM_COLS = 512;        // accumulators, two 64-column lo tiles, two 128-column update tiles
+constexpr int T_LO_COL = T_ACC_COLS;    // lo tiles (A operand of the lo MMAs)
+constexpr int T_UPD_COL = T_ACC_COLS + 2 * T_CK;  // update products D[c][r] (B steps)
+static_assert(T_UPD_COL + 2 * 128 <= T_TMEM_COLS, "TMEM plan exceeds the allocation");
 constexpr int T_DTS = 24;              // dT row stride (floats): conflict-free staging, 16-B rows
 
 struct TLayer {
@@ -168,7 +171,8 @@ __device__ void t_grid_sync(const TParams& P, u64& gen) {
 struct TSmem {
   float* ring;      // T_NSLOT x 32 KB (1024-B aligned)
   float* opnd;      // 2 x (hi, lo) x [M][64] no-swizzle K-major
-  float* dT;        // B: delta of the chunk rows, [2][64][M] (row-major by r), per operand buffer
+  float* dop;       // B: update MMA B operand [delta_hi; delta_lo]^T per chunk, [2][128][16]
+  float* aop;       // B: update MMA A operand a^T (hi, lo) of the unit's 128 columns, [2][128][16]
   float* red;       // 16 floats
   uint64_t* full;   // [T_NSLOT]
   uint64_t* sfree;  // [T_NSLOT] slot consumed (F: MMAs done; B: update done)
@@ -281,6 +285,8 @@ __device__ void t_mma(const TParams& P, const TSmem& sm, uint32_t tbase) {
         const TStep sp = t_step(P, S, st);
         const uint32_t id2 = tc_idesc_tf32(128, 2 * M, !sp.fwd, false);
         const uint32_t id1 = tc_idesc_tf32(128, M, false, false);  // A = lo tile in TMEM, K-major
+        const uint32_t idu2 = tc_idesc_tf32(128, 2 * T_CK, false, false), idu1 = tc_idesc_tf32(128, T_CK, false, false);
+        const bool upd = t_upd(P, P.t0 + ti, S.h);
         for (int u = c; u < sp.nunits; u += G, ++uc) {
           // consecutive K-steps go to T_NACC independent accumulators, so back-to-back
           // small-N MMAs do not wait on each other's accumulation
@@ -314,6 +320,20 @@ __device__ void t_mma(const TParams& P, const TSmem& sm, uint32_t tbase) {
 #pragma unroll
             for (int ks = 0; ks < T_CK / 8; ++ks)
               tc_mma_tf32_ts(acc + (ks % T_NACC) * 2 * M, lot + ks * 8, db + uint64_t(ks * 16), id1, true);
+            if (!sp.fwd && upd) {
+              // update product D[c][r] = sum_m a[m][c] delta[m][r] over K = m (2 K-steps):
+              // a_hi x [delta_hi; delta_lo] (N = 128) and a_lo x delta_hi (N = 64)
+              const uint64_t ua = tc_desc_kmajor_noswz(sm.aop, 0, T_MAXM);
+              const uint64_t ual = tc_desc_kmajor_noswz(sm.aop + 128 * T_MAXM, 0, T_MAXM);
+              const uint64_t ub = tc_desc_kmajor_noswz(sm.dop + size_t(b) * 2 * T_CK * T_MAXM, 0, T_MAXM);
+              const uint32_t ud = tbase + T_UPD_COL + uint32_t(b) * 128;
+#pragma unroll
+              for (int kk = 0; kk < T_MAXM / 8; ++kk)
+                tc_mma_tf32(ud, ua + uint64_t(kk * 16), ub + uint64_t(kk * 16), idu2, kk > 0);
+#pragma unroll
+              for (int kk = 0; kk < T_MAXM / 8; ++kk)
+                tc_mma_tf32(ud, ual + uint64_t(kk * 16), ub + uint64_t(kk * 16), idu1, true);
+            }
             tc_commit(&sm.mdone[b]);
             if (sp.fwd) tc_commit(&sm.sfree[slot]);
             t_trace(P, tr, 21);
@@ -341,7 +361,9 @@ struct TOpnd {
       v[q] = __ldcg(src + size_t(m) * ld + k);
     }
   }
-  __device__ __forceinline__ void put(float* ohi, float* olo, float* dT, int) const {
+  // dop != nullptr (B chunks): also the update MMA's B operand [delta_hi; delta_lo]^T, rows
+  // r (64 hi + 64 lo) x K = m (16), no-swizzle K-major (SBO 512 B)
+  __device__ __forceinline__ void put(float* ohi, float* olo, float* dop, int) const {
     const int st = threadIdx.x - T_SIMT0, lane = st & 31, w = st >> 5;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -350,7 +372,12 @@ struct TOpnd {
       const float h = tf32_hi(v[q]);
       ohi[off] = h;
       olo[off] = v[q] - h;
-      if (dT) dT[(kq * 4 + (lane & 3)) * T_DTS + mg * 8 + (lane >> 2)] = v[q];
+      if (dop) {
+        const int r = kq * 4 + (lane & 3), m = mg * 8 + (lane >> 2);
+        const int o2 = int(tc_kmajor_noswz_off(r, m, T_MAXM) >> 2);
+        dop[o2] = h;
+        dop[o2 + T_CK * T_MAXM] = v[q] - h;
+      }
     }
   }
 };
@@ -385,52 +412,54 @@ __device__ __forceinline__ int t_bofs(int cl, int r) {
   const int box = cl >> 5, g = (cl >> 3) & 3, e = cl & 7;
   return box * 2048 + r * 32 + ((g ^ (r & 3)) << 3) + e;
 }
-__device__ __forceinline__ void t_lo_update_pass(const float* tile, uint32_t lo_tmem, const float* dT,
-                                                 const float (&areg)[T_MAXM], float nlr, bool upd,
-                                                 float (&wn)[T_UPR]) {
+// lo^T of a B chunk into TMEM (the A operand of the lo MMAs)
+__device__ __forceinline__ void t_lo_pass_b(const float* tile, uint32_t lo_tmem) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cl = 32 * (warp & 3) + lane, rh = (warp - 2) >> 2;
   float v[32];
 #pragma unroll
   for (int rr = 0; rr < T_UPR; ++rr) {
-    const int r = rh * T_UPR + rr;
-    const float w = tile[t_bofs(cl, r)];
+    const float w = tile[t_bofs(cl, rh * T_UPR + rr)];
     v[rr] = w - tf32_hi(w);
-    if (upd) {
-      const float4* d4 = reinterpret_cast<const float4*>(dT + r * T_DTS);
-      float s0 = 0.f, s1 = 0.f;
-#pragma unroll
-      for (int q = 0; q < T_MAXM / 4; ++q) {
-        const float4 d = d4[q];
-        s0 = fmaf(d.x, areg[4 * q + 0], s0);
-        s1 = fmaf(d.y, areg[4 * q + 1], s1);
-        s0 = fmaf(d.z, areg[4 * q + 2], s0);
-        s1 = fmaf(d.w, areg[4 * q + 3], s1);
-      }
-      wn[rr] = fmaf(nlr, s0 + s1, w);
-    }
   }
   tmem_st_32x32b_x32(lo_tmem + ((uint32_t(32 * (warp & 3))) << 16) + uint32_t(32 * rh), v);
   tmem_st_wait();
 }
-__device__ __forceinline__ void t_write_back(float* tile, const float (&wn)[T_UPR]) {
+// In-place SGD step on a B chunk once all its MMAs are done: the tensor core has computed
+// D[c][r] = sum_m a[m][c] delta[m][r] (3xTF32, columns [0,64) hi*hi + lo*hi, [64,128) hi*lo);
+// thread = column c (its TMEM lane), 32 rows: w' = w - lr * (d0 + d1).
+__device__ __forceinline__ void t_apply_update(float* tile, uint32_t upd_tmem, float nlr) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cl = 32 * (warp & 3) + lane, rh = (warp - 2) >> 2;
+  const uint32_t ta = upd_tmem + ((uint32_t(32 * (warp & 3))) << 16) + uint32_t(32 * rh);
+  float d0[32], d1[32];
+  tmem_ld_32x32b_x32(ta, d0);
+  tmem_ld_32x32b_x32(ta + T_CK, d1);
+  float* colp[4];
 #pragma unroll
-  for (int rr = 0; rr < T_UPR; ++rr) tile[t_bofs(cl, rh * T_UPR + rr)] = wn[rr];
+  for (int x = 0; x < 4; ++x) colp[x] = tile + t_bofs(cl, x);
+#pragma unroll
+  for (int rr = 0; rr < T_UPR; ++rr) {
+    const int r = rh * T_UPR + rr;  // (r & 3) == (rr & 3)
+    float* p = colp[rr & 3] + (r - (rr & 3)) * 32;
+    *p = fmaf(nlr, d0[rr] + d1[rr], *p);
+  }
 }
 
 __global__ void __launch_bounds__(T_THREADS, 1) tile_kernel(const __grid_constant__ TParams P) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1024-B alignment of the swizzled tiles
-  unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // (pointer arithmetic on smem_raw, not integer casts, so the compiler keeps the shared
+  // state space and emits LDS/STS instead of generic loads)
+  unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   TSmem sm;
   const int M = P.M, G = P.G, c = blockIdx.x;
   const int ob = M * T_CK;
   sm.ring = reinterpret_cast<float*>(base);
   sm.opnd = sm.ring + T_NSLOT * T_SLOT_FLOATS;
-  sm.dT = sm.opnd + 2 * 2 * ob;
-  sm.red = sm.dT + 2 * T_CK * T_DTS;
+  sm.dop = sm.opnd + 2 * 2 * ob;
+  sm.aop = sm.dop + 2 * 2 * T_CK * T_MAXM;
+  sm.red = sm.aop + 2 * 128 * T_MAXM;
   sm.full = reinterpret_cast<uint64_t*>(sm.red + 16);
   sm.sfree = sm.full + T_NSLOT;
   sm.opnd_rdy = sm.sfree + T_NSLOT;
@@ -518,13 +547,19 @@ __global__ void __launch_bounds__(T_THREADS, 1) tile_kernel(const __grid_constan
           t_trace(P, tr, 1);
           for (int u = c; u < sp.nunits; u += G, ++uc) {
             const int blk = u / T_Q, q = u % T_Q;
-            float areg[T_MAXM];
             if (!sp.fwd && upd) {
-              // a_i[m][col] of this thread's update column, from the backward cache
-              const int col = blk * 128 + 32 * (warp & 3) + lane;  // t_lo_update_pass column
-#pragma unroll
-              for (int m = 0; m < T_MAXM; ++m)
-                areg[m] = m < M ? t_ld(Cb + L.a_in + size_t(m) * L.n_in + col) : 0.f;
+              // A operand of the update MMAs: a_i^T of the unit's 128 columns (backward cache),
+              // tf32 hi / lo, no-swizzle K-major [128][16]. Published with chunk 0's operands;
+              // the previous unit's MMAs are complete (its epilogue waited).
+              const int cbase = blk * 128;
+              for (int e = st_id; e < 128 * T_MAXM; e += T_NS) {
+                const int m = e >> 7, cc = e & 127;
+                const float x = t_ld(Cb + L.a_in + size_t(m) * L.n_in + cbase + cc);
+                const int o = int(tc_kmajor_noswz_off(cc, m, T_MAXM) >> 2);
+                const float h = tf32_hi(x);
+                sm.aop[o] = h;
+                sm.aop[128 * T_MAXM + o] = x - h;
+              }
             }
             // operand source of chunk ch: F = a_i[:, cols], B = delta[:, rows]
             const float* osrc;
@@ -543,14 +578,14 @@ __global__ void __launch_bounds__(T_THREADS, 1) tile_kernel(const __grid_constan
             for (int ch = 0; ch < sp.nchunks; ++ch, ++j) {
               const int slot = j % T_NSLOT, b = j & 1;
               float* tile = sm.ring + size_t(slot) * T_SLOT_FLOATS;
-              const uint32_t lot = tbase + T_ACC_COLS + uint32_t(b) * T_CK;  // lo tile in TMEM
+              const uint32_t lot = tbase + T_LO_COL + uint32_t(b) * T_CK;  // lo tile in TMEM
               float* ohi = sm.opnd + size_t(b) * 2 * ob;
-              float* dTb = sm.dT + size_t(b) * T_CK * T_DTS;
+              float* dopb = sm.dop + size_t(b) * 2 * T_CK * T_MAXM;
               t_trace(P, tr, 6);
-              if (j >= 2) t_wait(&sm.mdone[b], ((j - 2) >> 1) & 1, P);  // operand / lo buffer free
+              if (j >= 2) t_wait(&sm.mdone[b], ((j - 2) >> 1) & 1, P);  // operand / TMEM buffers free
               tc_fence_after();
               t_trace(P, tr, 11);
-              op.put(ohi, ohi + ob, sp.fwd ? nullptr : dTb, M);
+              op.put(ohi, ohi + ob, sp.fwd ? nullptr : dopb, M);
               if (ch + 1 < sp.nchunks) op.fetch(osrc + (ch + 1) * ostep, old, M);
               fence_proxy_async_shared();
               simt_sync();
@@ -558,35 +593,43 @@ __global__ void __launch_bounds__(T_THREADS, 1) tile_kernel(const __grid_constan
               t_trace(P, tr, 12);
               t_wait(&sm.full[slot], (j / T_NSLOT) & 1, P);
               t_trace(P, tr, 7);
-              if (sp.fwd) {
-                t_lo_pass_f(tile, lot);
-                t_trace(P, tr, 13);
-                tc_fence_before();
-                simt_sync();
-                if (st_id == 0) mbar_arrive(&sm.prep[b]);
-              } else {
-                float wn[T_UPR];
-                t_lo_update_pass(tile, lot, dTb, areg, nlr, upd, wn);
-                tc_fence_before();
-                simt_sync();
-                if (st_id == 0) mbar_arrive(&sm.prep[b]);
-                t_trace(P, tr, 8);
-                // the hi MMAs read the raw tile: write the update back only after them
-                t_wait(&sm.mhi[b], (j >> 1) & 1, P);
+              if (sp.fwd) t_lo_pass_f(tile, lot);
+              else t_lo_pass_b(tile, lot);
+              t_trace(P, tr, 13);
+              tc_fence_before();
+              simt_sync();
+              if (st_id == 0) mbar_arrive(&sm.prep[b]);
+              if (!sp.fwd && ch > 0) {
+                // previous chunk: all its MMAs (g_in reads of the raw tile, the update product)
+                // are done -> SGD step in place, then the producer stores the tile
+                const uint32_t jp = j - 1;
+                const int pslot = jp % T_NSLOT, bp = jp & 1;
+                t_wait(&sm.mdone[bp], (jp >> 1) & 1, P);
+                tc_fence_after();
                 t_trace(P, tr, 9);
                 if (upd) {
-                  t_write_back(tile, wn);
+                  t_apply_update(sm.ring + size_t(pslot) * T_SLOT_FLOATS, tbase + T_UPD_COL + uint32_t(bp) * 128, nlr);
                   fence_proxy_async_shared();
                 }
+                tc_fence_before();
                 simt_sync();
-                if (st_id == 0) mbar_arrive(&sm.sfree[slot]);
+                if (st_id == 0) mbar_arrive(&sm.sfree[pslot]);
                 t_trace(P, tr, 10);
               }
             }
-            // unit epilogue: last chunk's MMAs complete -> accumulator
+            // unit epilogue: last chunk's MMAs complete -> accumulator (and, in B, its update)
             const uint32_t jl = j - 1;
             t_wait(&sm.mdone[jl & 1], (jl >> 1) & 1, P);
             tc_fence_after();
+            if (!sp.fwd) {
+              const int slot = jl % T_NSLOT, bl = jl & 1;
+              if (upd) {
+                t_apply_update(sm.ring + size_t(slot) * T_SLOT_FLOATS, tbase + T_UPD_COL + uint32_t(bl) * 128, nlr);
+                fence_proxy_async_shared();
+              }
+              simt_sync();
+              if (st_id == 0) mbar_arrive(&sm.sfree[slot]);
+            }
             // TMEM -> partials: warps 2..5 cover lane quarters 2,3,0,1
             if (warp < 6) {
               const int lq = warp & 3;

@@ -6,7 +6,7 @@ from collections import defaultdict
 from paper_2210_09147_b200 import engine, model as mdl, streams
 
 NAMES = {1: "compute.begin", 2: "compute.end", 3: "barrier1", 4: "finalize", 5: "barrier2", 6: "chunk.begin",
-         7: "full.seen", 11: "mdone.j-2", 12: "opnd.rdy", 13: "lopass.end", 22: "mma.hi.issued", 23: "mma.prep.seen", 8: "prep.done", 9: "mdone.prev", 10: "update.done", 20: "mma.prep", 21: "mma.commit",
+         7: "full.seen", 11: "mdone.j-2", 12: "opnd.rdy", 13: "lopass.end", 22: "mma.hi.issued", 23: "mma.prep.seen", 8: "prep.done", 9: "mdone.prev", 10: "update.done", 14: "update.math", 20: "mma.prep", 21: "mma.commit",
          30: "tma.issue"}
 
 def run(widths, counts, ticks=2, M=16, learn=True, cta=0):
