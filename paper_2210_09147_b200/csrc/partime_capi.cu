@@ -155,7 +155,7 @@ struct pt_pipeline {
   std::vector<void*> allocs;
   u64* d_trace = nullptr;
   int trace_cap = 0, trace_cta = 0;
-  int pf_chunks = 0, split_bytes = 32768, maxfly = 0;  // tunables (env PT_PF_CHUNKS / PT_SPLIT_BYTES)
+  int pf_chunks = 0, split_bytes = 32768, maxfly = 0, wb_mode = 0;  // tunables (env PT_PF_CHUNKS / PT_SPLIT_BYTES)
   // shared-memory plan (see pt_kernels.cuh): ring slots first, then the small buffers
   int nslot = 0, slot_floats = 0, qw = 0, act_off = 0, spart_off = 0, spart_floats = 0, delta_off = 0,
       red_off = 0, scal_off = 0, bar_off = 0, flags_off = 0, desc_off = 0, bias_off = 0, smem_bytes = 0;
@@ -490,6 +490,7 @@ int create_impl(const pt_config* c, pt_pipeline* p) {
   if (const char* e = getenv("PT_PF_CHUNKS")) p->pf_chunks = std::max(0, atoi(e));
   if (const char* e = getenv("PT_DBG")) p->dbg = atoi(e);
   if (const char* e = getenv("PT_POLICY")) p->policy = atoi(e);
+  if (const char* e = getenv("PT_WB")) p->wb_mode = atoi(e) ? 1 : 0;
   if (const char* e = getenv("PT_SPLIT_BYTES")) p->split_bytes = std::max(1024, atoi(e)) / 16 * 16;
 
   CUDA_TRY(cudaGetDevice(&p->device));
@@ -738,6 +739,7 @@ int run_impl(pt_pipeline* p, const float* xs, const float* ys, int64_t n, float*
   P.pf_chunks = p->pf_chunks;
   P.split_bytes = p->split_bytes;
   P.maxfly = p->maxfly;
+  P.wb_mode = p->wb_mode;
   P.dbg = p->dbg;
   P.policy = p->policy;
   P.trace = p->d_trace;

@@ -90,16 +90,18 @@ struct TParams {
   int trace_cap, trace_cta;
 };
 
-// SIMT thread 0 writes [0, cap/2), the MMA thread [cap/2, 3cap/4), the producer [3cap/4, cap)
+// SIMT group A thread 0 writes [0, cap/4), group B thread 0 [cap/4, cap/2), the MMA
+// thread [cap/2, 3cap/4), the producer [3cap/4, cap)
 __device__ __forceinline__ void t_trace(const TParams& P, int& idx, int code) {
   if (P.trace == nullptr || blockIdx.x != P.trace_cta) return;
-  const int tid = threadIdx.x;
-  int lo, hi;
-  if (tid == T_SIMT0) { lo = 0; hi = P.trace_cap / 2; }
-  else if (tid == 32) { lo = P.trace_cap / 2; hi = P.trace_cap - P.trace_cap / 4; }
-  else if (tid == 0) { lo = P.trace_cap - P.trace_cap / 4; hi = P.trace_cap; }
+  const int tid = threadIdx.x, q = P.trace_cap / 4;
+  int lo;
+  if (tid == T_SIMT0) lo = 0;
+  else if (tid == T_SIMT0 + 128) lo = q;
+  else if (tid == 32) lo = 2 * q;
+  else if (tid == 0) lo = 3 * q;
   else return;
-  if (lo + idx < hi) P.trace[lo + idx++] = (u64(code) << 56) | (globaltimer() & 0x00FFFFFFFFFFFFFFull);
+  if (idx < q) P.trace[lo + idx++] = (u64(code) << 56) | (globaltimer() & 0x00FFFFFFFFFFFFFFull);
 }
 
 // ------------------------------------------------------------------ schedule
@@ -147,6 +149,13 @@ __device__ __forceinline__ void t_wait(uint64_t* bar, uint32_t parity, const TPa
     if (t_watch(P, t0)) return;
 }
 __device__ __forceinline__ void simt_sync() { asm volatile("bar.sync 1, %0;" ::"n"(T_NS) : "memory"); }
+// SIMT group A (warps 2-5: operands, lo tiles, accumulator epilogue) and group B (warps 6-9:
+// SGD write-back of backward tiles); each covers the four TMEM lane quarters once
+constexpr int T_GRP = T_NS / 2;
+__device__ __forceinline__ void grp_sync(int g) {
+  if (g == 0) asm volatile("bar.sync 2, %0;" ::"n"(T_GRP) : "memory");
+  else asm volatile("bar.sync 3, %0;" ::"n"(T_GRP) : "memory");
+}
 __device__ __forceinline__ float t_ld(const float* p) { return __ldcg(p); }
 __device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
 
@@ -181,6 +190,7 @@ struct TSmem {
   uint64_t* mhi;    // [2] hi MMAs of the chunk done (raw tile no longer read)
   uint64_t* mdone;  // [2] all MMAs of the chunk done
   uint64_t* afree;  // [2] accumulator read by the epilogue
+  uint64_t* applied;  // [2] update product of a backward chunk consumed (TMEM buffer free)
   uint32_t* tmem;
 };
 
@@ -276,7 +286,7 @@ __device__ void t_mma(const TParams& P, const TSmem& sm, uint32_t tbase) {
   // The hi MMAs read the raw TMA tile (the tensor core uses its top 19 bits = tf32(w)),
   // so they start as soon as the tile lands; the lo MMAs wait for the SIMT split.
   const int c = blockIdx.x, G = P.G, M = P.M;
-  uint32_t j = 0, uc = 0;  // chunk, unit counters
+  uint32_t j = 0, uc = 0, bj = 0;  // chunk, unit, backward-chunk counters
   int tr = 0;
   for (int ti = 0; ti < P.n; ++ti) {
     for (int s = 0; s < P.n_stages; ++s) {
@@ -288,51 +298,48 @@ __device__ void t_mma(const TParams& P, const TSmem& sm, uint32_t tbase) {
         const uint32_t idu2 = tc_idesc_tf32(128, 2 * T_CK, false, false), idu1 = tc_idesc_tf32(128, T_CK, false, false);
         const bool upd = t_upd(P, P.t0 + ti, S.h);
         for (int u = c; u < sp.nunits; u += G, ++uc) {
-          // consecutive K-steps go to T_NACC independent accumulators, so back-to-back
-          // small-N MMAs do not wait on each other's accumulation
           const uint32_t acc = tbase + (uc & 1) * uint32_t(T_NACC * 2 * M);
-          (void)0;
           if (uc >= 2) t_wait(&sm.afree[uc & 1], ((uc - 2) >> 1) & 1, P);
           for (int ch = 0; ch < sp.nchunks; ++ch, ++j) {
             const int slot = j % T_NSLOT, b = j & 1;
             const float* hi = sm.ring + size_t(slot) * T_SLOT_FLOATS;
             const float* opn = sm.opnd + size_t(b) * 2 * M * T_CK;
-            t_wait(&sm.opnd_rdy[b], (j >> 1) & 1, P);
+            t_wait(&sm.prep[b], (j >> 1) & 1, P);  // operands and the lo tile
             t_wait(&sm.full[slot], (j / T_NSLOT) & 1, P);
             t_trace(P, tr, 20);
             tc_fence_after();
             // descriptors advance by constants per K-step (start-address field, 16-B units):
             // K-major SW128: +32 B inside the 128-B atom, +16 KB to the next 32-column box;
             // MN-major SW128_32B: +8 rows = 1 KB; operand (no swizzle): +256 B
-            uint64_t da = sp.fwd ? tc_desc_kmajor_sw128(hi, 0) : tc_desc_mn_sw128b32(hi, 0, 8192);
-            uint64_t db = tc_desc_kmajor_noswz(opn, 0, T_CK);
+            const uint64_t da = sp.fwd ? tc_desc_kmajor_sw128(hi, 0) : tc_desc_mn_sw128b32(hi, 0, 8192);
+            const uint64_t db = tc_desc_kmajor_noswz(opn, 0, T_CK);
+            const uint32_t lot = tbase + T_LO_COL + uint32_t(b) * T_CK;  // lo tile in TMEM
 #pragma unroll
             for (int ks = 0; ks < T_CK / 8; ++ks) {
               const uint64_t dak = sp.fwd ? da + uint64_t((ks >> 2) * 1024 + (ks & 3) * 2) : da + uint64_t(ks * 64);
-              tc_mma_tf32(acc + (ks % T_NACC) * 2 * M, dak, db + uint64_t(ks * 16), id2, ch > 0 || ks >= T_NACC);
+              tc_mma_tf32(acc, dak, db + uint64_t(ks * 16), id2, ch > 0 || ks > 0);
+              tc_mma_tf32_ts(acc, lot + ks * 8, db + uint64_t(ks * 16), id1, true);
             }
-            tc_commit(&sm.mhi[b]);
-            t_trace(P, tr, 22);
-            t_wait(&sm.prep[b], (j >> 1) & 1, P);
-            t_trace(P, tr, 23);
-            tc_fence_after();
-            const uint32_t lot = tbase + T_ACC_COLS + uint32_t(b) * T_CK;  // lo tile in TMEM
+            if (!sp.fwd) {
+              // the update product goes to TMEM buffer bj % 2, free once group B applied bj - 2
+              const uint32_t ubuf = bj & 1;
+              if (bj >= 2) t_wait(&sm.applied[ubuf], ((bj - 2) >> 1) & 1, P);
+              tc_fence_after();
+              if (upd) {
+                // D[c][r] = sum_m a[m][c] delta[m][r] over K = m (2 K-steps):
+                // a_hi x [delta_hi; delta_lo] (N = 128) and a_lo x delta_hi (N = 64)
+                const uint64_t ua = tc_desc_kmajor_noswz(sm.aop, 0, T_MAXM);
+                const uint64_t ual = tc_desc_kmajor_noswz(sm.aop + 128 * T_MAXM, 0, T_MAXM);
+                const uint64_t ub = tc_desc_kmajor_noswz(sm.dop + size_t(b) * 2 * T_CK * T_MAXM, 0, T_MAXM);
+                const uint32_t ud = tbase + T_UPD_COL + ubuf * 128;
 #pragma unroll
-            for (int ks = 0; ks < T_CK / 8; ++ks)
-              tc_mma_tf32_ts(acc + (ks % T_NACC) * 2 * M, lot + ks * 8, db + uint64_t(ks * 16), id1, true);
-            if (!sp.fwd && upd) {
-              // update product D[c][r] = sum_m a[m][c] delta[m][r] over K = m (2 K-steps):
-              // a_hi x [delta_hi; delta_lo] (N = 128) and a_lo x delta_hi (N = 64)
-              const uint64_t ua = tc_desc_kmajor_noswz(sm.aop, 0, T_MAXM);
-              const uint64_t ual = tc_desc_kmajor_noswz(sm.aop + 128 * T_MAXM, 0, T_MAXM);
-              const uint64_t ub = tc_desc_kmajor_noswz(sm.dop + size_t(b) * 2 * T_CK * T_MAXM, 0, T_MAXM);
-              const uint32_t ud = tbase + T_UPD_COL + uint32_t(b) * 128;
+                for (int kk = 0; kk < T_MAXM / 8; ++kk)
+                  tc_mma_tf32(ud, ua + uint64_t(kk * 16), ub + uint64_t(kk * 16), idu2, kk > 0);
 #pragma unroll
-              for (int kk = 0; kk < T_MAXM / 8; ++kk)
-                tc_mma_tf32(ud, ua + uint64_t(kk * 16), ub + uint64_t(kk * 16), idu2, kk > 0);
-#pragma unroll
-              for (int kk = 0; kk < T_MAXM / 8; ++kk)
-                tc_mma_tf32(ud, ual + uint64_t(kk * 16), ub + uint64_t(kk * 16), idu1, true);
+                for (int kk = 0; kk < T_MAXM / 8; ++kk)
+                  tc_mma_tf32(ud, ual + uint64_t(kk * 16), ub + uint64_t(kk * 16), idu1, true);
+              }
+              ++bj;
             }
             tc_commit(&sm.mdone[b]);
             if (sp.fwd) tc_commit(&sm.sfree[slot]);
@@ -350,14 +357,15 @@ __device__ void t_mma(const TParams& P, const TSmem& sm, uint32_t tbase) {
 // chunk j is processed: fetch() issues the loads into registers, put() stores them.
 // With dT != nullptr (B chunks), the exact values are also kept as dT[k][m] for the update.
 struct TOpnd {
-  // thread -> 4 elements (m, k): lane = (m % 8) * 4 + k % 4, so every warp store of the
-  // no-swizzle core-matrix layout hits 32 distinct banks (M == 16: 2 row groups x 16 k-quads)
-  float v[4];
+  // group A thread -> 8 elements (m, k): lane = (m % 8) * 4 + k % 4, so every warp store of
+  // the no-swizzle core-matrix layout hits 32 distinct banks (M == 16: 2 row groups x 16
+  // k-quads)
+  float v[8];
   __device__ __forceinline__ void fetch(const float* src, int ld, int) {
     const int st = threadIdx.x - T_SIMT0, lane = st & 31, w = st >> 5;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int idx = w * 4 + q, m = (idx & 1) * 8 + (lane >> 2), k = (idx >> 1) * 4 + (lane & 3);
+    for (int q = 0; q < 8; ++q) {
+      const int idx = w * 8 + q, m = (idx & 1) * 8 + (lane >> 2), k = (idx >> 1) * 4 + (lane & 3);
       v[q] = __ldcg(src + size_t(m) * ld + k);
     }
   }
@@ -366,8 +374,8 @@ struct TOpnd {
   __device__ __forceinline__ void put(float* ohi, float* olo, float* dop, int) const {
     const int st = threadIdx.x - T_SIMT0, lane = st & 31, w = st >> 5;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int idx = w * 4 + q, mg = idx & 1, kq = idx >> 1;
+    for (int q = 0; q < 8; ++q) {
+      const int idx = w * 8 + q, mg = idx & 1, kq = idx >> 1;
       const int off = mg * 512 + kq * 32 + lane;  // == tc_kmajor_noswz_off(m, k, 64) / 4
       const float h = tf32_hi(v[q]);
       ohi[off] = h;
@@ -383,66 +391,77 @@ struct TOpnd {
 };
 
 // The lo tile (w - tf32(w)) goes straight from registers to TMEM (tcgen05.st), where the
-// lo MMAs read it as their A operand: lane = M row, column = K element. SIMT warp w owns
-// TMEM lanes 32 * (w % 4) .. +31 and the K half (w - 2) / 4 of the 64-deep chunk.
+// lo MMAs read it as their A operand: lane = M row, column = K element. A group-A warp
+// owns TMEM lanes 32 * (warp % 4) .. +31 and both 32-deep K halves of the 64-deep chunk.
 //
-// F chunk (K-major SWIZZLE_128B tile, 2 boxes [128 rows][32 cols]): thread = W row r, 32 k.
+// F chunk (K-major SWIZZLE_128B tile, 2 boxes [128 rows][32 cols]): thread = W row r.
 __device__ __forceinline__ void t_lo_pass_f(const float* tile, uint32_t lo_tmem) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int r = 32 * (warp & 3) + lane, kh = (warp - 2) >> 2;
-  const float* row = tile + kh * 4096 + r * 32;
-  float v[32];
+  const int r = 32 * (warp & 3) + lane;
 #pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    const float4 w = *reinterpret_cast<const float4*>(row + ((c ^ (r & 7)) << 2));
-    v[4 * c + 0] = w.x - tf32_hi(w.x);
-    v[4 * c + 1] = w.y - tf32_hi(w.y);
-    v[4 * c + 2] = w.z - tf32_hi(w.z);
-    v[4 * c + 3] = w.w - tf32_hi(w.w);
+  for (int kh = 0; kh < 2; ++kh) {
+    const float* row = tile + kh * 4096 + r * 32;
+    float v[32];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const float4 w = *reinterpret_cast<const float4*>(row + ((c ^ (r & 7)) << 2));
+      v[4 * c + 0] = w.x - tf32_hi(w.x);
+      v[4 * c + 1] = w.y - tf32_hi(w.y);
+      v[4 * c + 2] = w.z - tf32_hi(w.z);
+      v[4 * c + 3] = w.w - tf32_hi(w.w);
+    }
+    tmem_st_32x32b_x32(lo_tmem + ((uint32_t(32 * (warp & 3))) << 16) + uint32_t(32 * kh), v);
   }
-  tmem_st_32x32b_x32(lo_tmem + ((uint32_t(32 * (warp & 3))) << 16) + uint32_t(32 * kh), v);
   tmem_st_wait();
 }
 
-// B chunk on the ATOM_32B tile [64 rows][4 boxes x 32 cols]: thread = W column c (the A
-// row of W^T), 32 rows. lo^T goes to TMEM; with upd, the SGD step
-// w' = w - lr * sum_m dT[r][m] a[m][c] is kept in registers for t_write_back.
-constexpr int T_UPR = 32;  // rows per thread
+// B chunk on the ATOM_32B tile [64 rows][4 boxes x 32 cols]: thread = W column c (the A row
+// of W^T), 64 rows; the swizzle permutes 32-B granules by row & 3.
+constexpr int T_UPR = 32;  // rows per TMEM store
 __device__ __forceinline__ int t_bofs(int cl, int r) {
   const int box = cl >> 5, g = (cl >> 3) & 3, e = cl & 7;
   return box * 2048 + r * 32 + ((g ^ (r & 3)) << 3) + e;
 }
-// lo^T of a B chunk into TMEM (the A operand of the lo MMAs)
 __device__ __forceinline__ void t_lo_pass_b(const float* tile, uint32_t lo_tmem) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int cl = 32 * (warp & 3) + lane, rh = (warp - 2) >> 2;
-  float v[32];
+  const int cl = 32 * (warp & 3) + lane;
+  const float* colp[4];
 #pragma unroll
-  for (int rr = 0; rr < T_UPR; ++rr) {
-    const float w = tile[t_bofs(cl, rh * T_UPR + rr)];
-    v[rr] = w - tf32_hi(w);
+  for (int x = 0; x < 4; ++x) colp[x] = tile + t_bofs(cl, x);
+#pragma unroll
+  for (int rh = 0; rh < 2; ++rh) {
+    float v[32];
+#pragma unroll
+    for (int rr = 0; rr < T_UPR; ++rr) {
+      const float w = colp[rr & 3][(rh * T_UPR + rr - (rr & 3)) * 32];
+      v[rr] = w - tf32_hi(w);
+    }
+    tmem_st_32x32b_x32(lo_tmem + ((uint32_t(32 * (warp & 3))) << 16) + uint32_t(32 * rh), v);
   }
-  tmem_st_32x32b_x32(lo_tmem + ((uint32_t(32 * (warp & 3))) << 16) + uint32_t(32 * rh), v);
   tmem_st_wait();
 }
-// In-place SGD step on a B chunk once all its MMAs are done: the tensor core has computed
-// D[c][r] = sum_m a[m][c] delta[m][r] (3xTF32, columns [0,64) hi*hi + lo*hi, [64,128) hi*lo);
-// thread = column c (its TMEM lane), 32 rows: w' = w - lr * (d0 + d1).
+// In-place SGD step on a B chunk once all its MMAs are done (group B): the tensor core has
+// computed D[c][r] = sum_m a[m][c] delta[m][r] (3xTF32, columns [0,64) hi*hi + lo*hi,
+// [64,128) hi*lo); thread = column c (its TMEM lane), 64 rows: w' = w - lr * (d0 + d1).
 __device__ __forceinline__ void t_apply_update(float* tile, uint32_t upd_tmem, float nlr) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int cl = 32 * (warp & 3) + lane, rh = (warp - 2) >> 2;
-  const uint32_t ta = upd_tmem + ((uint32_t(32 * (warp & 3))) << 16) + uint32_t(32 * rh);
-  float d0[32], d1[32];
-  tmem_ld_32x32b_x32(ta, d0);
-  tmem_ld_32x32b_x32(ta + T_CK, d1);
+  const int cl = 32 * (warp & 3) + lane;
   float* colp[4];
 #pragma unroll
   for (int x = 0; x < 4; ++x) colp[x] = tile + t_bofs(cl, x);
 #pragma unroll
-  for (int rr = 0; rr < T_UPR; ++rr) {
-    const int r = rh * T_UPR + rr;  // (r & 3) == (rr & 3)
-    float* p = colp[rr & 3] + (r - (rr & 3)) * 32;
-    *p = fmaf(nlr, d0[rr] + d1[rr], *p);
+  for (int rh = 0; rh < 2; ++rh) {
+    const uint32_t ta = upd_tmem + ((uint32_t(32 * (warp & 3))) << 16) + uint32_t(32 * rh);
+    float d0[32], d1[32];
+    tmem_ld_2x32(ta, ta + T_CK, d0, d1);
+    // all loads before any store: the compiler cannot prove the rows distinct, and a
+    // load-after-store chain would serialize on shared-memory latency
+    float w[T_UPR];
+#pragma unroll
+    for (int rr = 0; rr < T_UPR; ++rr) w[rr] = colp[rr & 3][(rh * T_UPR + rr - (rr & 3)) * 32];
+#pragma unroll
+    for (int rr = 0; rr < T_UPR; ++rr)
+      colp[rr & 3][(rh * T_UPR + rr - (rr & 3)) * 32] = fmaf(nlr, d0[rr] + d1[rr], w[rr]);
   }
 }
 
@@ -467,7 +486,8 @@ __global__ void __launch_bounds__(T_THREADS, 1) tile_kernel(const __grid_constan
   sm.mhi = sm.prep + 2;
   sm.mdone = sm.mhi + 2;
   sm.afree = sm.mdone + 2;
-  sm.tmem = reinterpret_cast<uint32_t*>(sm.afree + 2);
+  sm.applied = sm.afree + 2;
+  sm.tmem = reinterpret_cast<uint32_t*>(sm.applied + 2);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     for (int s = 0; s < T_NSLOT; ++s) {
@@ -480,6 +500,7 @@ __global__ void __launch_bounds__(T_THREADS, 1) tile_kernel(const __grid_constan
       mbar_init(&sm.prep[b], 1);
       mbar_init(&sm.mdone[b], 1);
       mbar_init(&sm.afree[b], 1);
+      mbar_init(&sm.applied[b], 1);
     }
     fence_mbar_init();
   }
@@ -499,7 +520,7 @@ __global__ void __launch_bounds__(T_THREADS, 1) tile_kernel(const __grid_constan
     const int gtid = c * T_NS + st_id, gthreads = G * T_NS;
     const float nlr = -P.lr;
     const float inv_mf = 1.f / float(M * P.F);
-    uint32_t j = 0, uc = 0;
+    uint32_t j = 0, uc = 0, bj = 0;
     u64 gen = 0;
     int tr = 0;
     for (int ti = 0; ti < P.n; ++ti) {
@@ -545,116 +566,103 @@ __global__ void __launch_bounds__(T_THREADS, 1) tile_kernel(const __grid_constan
             }
           }
           t_trace(P, tr, 1);
+          const int grp = warp < 6 ? 0 : 1;
           for (int u = c; u < sp.nunits; u += G, ++uc) {
             const int blk = u / T_Q, q = u % T_Q;
-            if (!sp.fwd && upd) {
-              // A operand of the update MMAs: a_i^T of the unit's 128 columns (backward cache),
-              // tf32 hi / lo, no-swizzle K-major [128][16]. Published with chunk 0's operands;
-              // the previous unit's MMAs are complete (its epilogue waited).
-              const int cbase = blk * 128;
-              for (int e = st_id; e < 128 * T_MAXM; e += T_NS) {
-                const int m = e >> 7, cc = e & 127;
-                const float x = t_ld(Cb + L.a_in + size_t(m) * L.n_in + cbase + cc);
-                const int o = int(tc_kmajor_noswz_off(cc, m, T_MAXM) >> 2);
-                const float h = tf32_hi(x);
-                sm.aop[o] = h;
-                sm.aop[128 * T_MAXM + o] = x - h;
-              }
-            }
-            // operand source of chunk ch: F = a_i[:, cols], B = delta[:, rows]
-            const float* osrc;
-            int old, ostep;
-            if (sp.fwd) {
-              const int c0 = q * (L.n_in / T_Q);
-              osrc = (i == 0) ? in + c0 : Ccur + L.a_in + c0;
-              old = (i == 0) ? ld_in0 : L.n_in;
-            } else {
-              osrc = P.delta + q * (L.n_out / T_Q);
-              old = P.max_n;
-            }
-            ostep = T_CK;
-            TOpnd op;
-            op.fetch(osrc, old, M);
-            for (int ch = 0; ch < sp.nchunks; ++ch, ++j) {
-              const int slot = j % T_NSLOT, b = j & 1;
-              float* tile = sm.ring + size_t(slot) * T_SLOT_FLOATS;
-              const uint32_t lot = tbase + T_LO_COL + uint32_t(b) * T_CK;  // lo tile in TMEM
-              float* ohi = sm.opnd + size_t(b) * 2 * ob;
-              float* dopb = sm.dop + size_t(b) * 2 * T_CK * T_MAXM;
-              t_trace(P, tr, 6);
-              if (j >= 2) t_wait(&sm.mdone[b], ((j - 2) >> 1) & 1, P);  // operand / TMEM buffers free
-              tc_fence_after();
-              t_trace(P, tr, 11);
-              op.put(ohi, ohi + ob, sp.fwd ? nullptr : dopb, M);
-              if (ch + 1 < sp.nchunks) op.fetch(osrc + (ch + 1) * ostep, old, M);
-              fence_proxy_async_shared();
-              simt_sync();
-              if (st_id == 0) mbar_arrive(&sm.opnd_rdy[b]);
-              t_trace(P, tr, 12);
-              t_wait(&sm.full[slot], (j / T_NSLOT) & 1, P);
-              t_trace(P, tr, 7);
-              if (sp.fwd) t_lo_pass_f(tile, lot);
-              else t_lo_pass_b(tile, lot);
-              t_trace(P, tr, 13);
-              tc_fence_before();
-              simt_sync();
-              if (st_id == 0) mbar_arrive(&sm.prep[b]);
-              if (!sp.fwd && ch > 0) {
-                // previous chunk: all its MMAs (g_in reads of the raw tile, the update product)
-                // are done -> SGD step in place, then the producer stores the tile
-                const uint32_t jp = j - 1;
-                const int pslot = jp % T_NSLOT, bp = jp & 1;
-                t_wait(&sm.mdone[bp], (jp >> 1) & 1, P);
-                tc_fence_after();
-                t_trace(P, tr, 9);
-                if (upd) {
-                  t_apply_update(sm.ring + size_t(pslot) * T_SLOT_FLOATS, tbase + T_UPD_COL + uint32_t(bp) * 128, nlr);
-                  fence_proxy_async_shared();
+            if (grp == 0) {
+              // ===================== group A: operands, lo tiles, accumulator epilogue
+              if (!sp.fwd && upd) {
+                // A operand of the update MMAs: a_i^T of the unit's 128 columns (backward
+                // cache), tf32 hi / lo, no-swizzle K-major [128][16]; published with chunk
+                // 0's prep. The previous unit's MMAs are complete (its epilogue waited).
+                const int cbase = blk * 128;
+                for (int e = st_id; e < 128 * T_MAXM; e += T_GRP) {
+                  const int m = e >> 7, cc = e & 127;
+                  const float x = t_ld(Cb + L.a_in + size_t(m) * L.n_in + cbase + cc);
+                  const int o = int(tc_kmajor_noswz_off(cc, m, T_MAXM) >> 2);
+                  const float h = tf32_hi(x);
+                  sm.aop[o] = h;
+                  sm.aop[128 * T_MAXM + o] = x - h;
                 }
+              }
+              // operand source of chunk ch: F = a_i[:, cols], B = delta[:, rows]
+              const float* osrc;
+              int old;
+              if (sp.fwd) {
+                const int c0 = q * (L.n_in / T_Q);
+                osrc = (i == 0) ? in + c0 : Ccur + L.a_in + c0;
+                old = (i == 0) ? ld_in0 : L.n_in;
+              } else {
+                osrc = P.delta + q * (L.n_out / T_Q);
+                old = P.max_n;
+              }
+              TOpnd op;
+              op.fetch(osrc, old, M);
+              for (int ch = 0; ch < sp.nchunks; ++ch, ++j) {
+                const int slot = j % T_NSLOT, b = j & 1;
+                const float* tile = sm.ring + size_t(slot) * T_SLOT_FLOATS;
+                const uint32_t lot = tbase + T_LO_COL + uint32_t(b) * T_CK;  // lo tile in TMEM
+                float* ohi = sm.opnd + size_t(b) * 2 * ob;
+                float* dopb = sm.dop + size_t(b) * 2 * T_CK * T_MAXM;
+                t_trace(P, tr, 6);
+                if (j >= 2) t_wait(&sm.mdone[b], ((j - 2) >> 1) & 1, P);  // operand / TMEM buffers free
+                tc_fence_after();
+                op.put(ohi, ohi + ob, sp.fwd ? nullptr : dopb, M);
+                if (ch + 1 < sp.nchunks) op.fetch(osrc + (ch + 1) * T_CK, old, M);
+                t_wait(&sm.full[slot], (j / T_NSLOT) & 1, P);
+                t_trace(P, tr, 7);
+                if (sp.fwd) t_lo_pass_f(tile, lot);
+                else t_lo_pass_b(tile, lot);
+                t_trace(P, tr, 13);
+                fence_proxy_async_shared();  // operands -> the tensor core (async proxy)
                 tc_fence_before();
-                simt_sync();
-                if (st_id == 0) mbar_arrive(&sm.sfree[pslot]);
-                t_trace(P, tr, 10);
+                grp_sync(0);
+                if (st_id == 0) mbar_arrive(&sm.prep[b]);
+              }
+              // unit epilogue: last chunk's MMAs complete -> accumulator -> quarter partials
+              const uint32_t jl = j - 1;
+              t_wait(&sm.mdone[jl & 1], (jl >> 1) & 1, P);
+              tc_fence_after();
+              {
+                const int lq = warp & 3;
+                const uint32_t ta = tbase + (uc & 1) * uint32_t(T_NACC * 2 * M) + ((uint32_t(lq) * 32) << 16);
+                float v[16], vv[32];
+                tmem_ld_32x32b_x32(ta, vv);  // one load + wait: columns [0,16) and [16,32)
+#pragma unroll
+                for (int m = 0; m < 16; ++m) v[m] = vv[m] + vv[16 + m];  // (hi + lo) * a_hi + hi * a_lo
+                const int rowcol = blk * 128 + lq * 32 + lane;  // F: output row; B: input column
+                float* dst = P.part + size_t(q) * M * P.max_n + rowcol;
+#pragma unroll
+                for (int m = 0; m < 16; ++m) dst[size_t(m) * P.max_n] = v[m];
+              }
+              tc_fence_before();
+              grp_sync(0);
+              if (st_id == 0) mbar_arrive(&sm.afree[uc & 1]);
+            } else {
+              // ===================== group B: SGD write-back of the backward tiles
+              if (sp.fwd) {
+                j += sp.nchunks;
+              } else {
+                for (int ch = 0; ch < sp.nchunks; ++ch, ++j, ++bj) {
+                  const int slot = j % T_NSLOT, b = j & 1;
+                  t_trace(P, tr, 8);
+                  t_wait(&sm.mdone[b], (j >> 1) & 1, P);
+                  tc_fence_after();
+                  t_trace(P, tr, 9);
+                  if (upd) {
+                    t_apply_update(sm.ring + size_t(slot) * T_SLOT_FLOATS, tbase + T_UPD_COL + (bj & 1) * 128, nlr);
+                    fence_proxy_async_shared();  // W' -> the producer's TMA store
+                  }
+                  tc_fence_before();
+                  grp_sync(1);
+                  if (st_id == T_GRP) {
+                    mbar_arrive(&sm.sfree[slot]);
+                    mbar_arrive(&sm.applied[bj & 1]);
+                  }
+                  t_trace(P, tr, 10);
+                }
               }
             }
-            // unit epilogue: last chunk's MMAs complete -> accumulator (and, in B, its update)
-            const uint32_t jl = j - 1;
-            t_wait(&sm.mdone[jl & 1], (jl >> 1) & 1, P);
-            tc_fence_after();
-            if (!sp.fwd) {
-              const int slot = jl % T_NSLOT, bl = jl & 1;
-              if (upd) {
-                t_apply_update(sm.ring + size_t(slot) * T_SLOT_FLOATS, tbase + T_UPD_COL + uint32_t(bl) * 128, nlr);
-                fence_proxy_async_shared();
-              }
-              simt_sync();
-              if (st_id == 0) mbar_arrive(&sm.sfree[slot]);
-            }
-            // TMEM -> partials: warps 2..5 cover lane quarters 2,3,0,1
-            if (warp < 6) {
-              const int lq = warp & 3;
-              const uint32_t ta = tbase + (uc & 1) * uint32_t(T_NACC * 2 * M) + ((uint32_t(lq) * 32) << 16);
-              float v[16], v2[16];
-              tmem_ld_32x32b_x16(ta, v);
-              tmem_ld_32x32b_x16(ta + 16, v2);
-#pragma unroll
-              for (int m = 0; m < 16; ++m) v[m] += v2[m];  // (hi + lo) * a_hi + hi * a_lo
-              for (int a = 1; a < T_NACC; ++a) {
-                tmem_ld_32x32b_x16(ta + a * 32, v2);
-#pragma unroll
-                for (int m = 0; m < 16; ++m) v[m] += v2[m];
-                tmem_ld_32x32b_x16(ta + a * 32 + 16, v2);
-#pragma unroll
-                for (int m = 0; m < 16; ++m) v[m] += v2[m];
-              }
-              const int rowcol = blk * 128 + lq * 32 + lane;  // F: output row; B: input column
-              float* dst = P.part + size_t(q) * M * P.max_n + rowcol;
-#pragma unroll
-              for (int m = 0; m < 16; ++m) dst[size_t(m) * P.max_n] = v[m];
-            }
-            tc_fence_before();
-            simt_sync();
-            if (st_id == 0) mbar_arrive(&sm.afree[uc & 1]);
           }
           t_trace(P, tr, 2);
           t_grid_sync(P, gen);

@@ -6,7 +6,7 @@ from collections import defaultdict
 from paper_2210_09147_b200 import engine, model as mdl, streams
 
 NAMES = {1: "compute.begin", 2: "compute.end", 3: "barrier1", 4: "finalize", 5: "barrier2", 6: "chunk.begin",
-         7: "full.seen", 11: "mdone.j-2", 12: "opnd.rdy", 13: "lopass.end", 22: "mma.hi.issued", 23: "mma.prep.seen", 8: "prep.done", 9: "mdone.prev", 10: "update.done", 14: "update.math", 20: "mma.prep", 21: "mma.commit",
+         7: "full.seen", 11: "mdone.j-2", 12: "opnd.rdy", 13: "lopass.end", 22: "mma.hi.issued", 23: "mma.prep.seen", 8: "prep.done", 8: "grpB.wait", 9: "grpB.mdone", 10: "grpB.done", 14: "update.math", 20: "mma.prep", 21: "mma.commit",
          30: "tma.issue"}
 
 def run(widths, counts, ticks=2, M=16, learn=True, cta=0):
@@ -20,7 +20,21 @@ def run(widths, counts, ticks=2, M=16, learn=True, cta=0):
     p.set_trace(cta, 1 << 14)
     p.run(xs, ys); p.sync()
     ms = p.last_kernel_ms()
-    cons, mma, prod = p.get_trace()
+    import ctypes
+    from paper_2210_09147_b200 import _lib as L_
+    cap = p._trace_cap
+    buf = np.zeros(cap, np.uint64)
+    L_.check(p._lib.pt_get_trace(p._h, buf.ctypes.data_as(ctypes.c_void_p), cap), "get_trace")
+    dec = lambda a: [(int(v >> np.uint64(56)), int(v & np.uint64(0x00FFFFFFFFFFFFFF))) for v in a if v]
+    q4 = cap // 4
+    cons, grpb, mma, prod = dec(buf[:q4]), dec(buf[q4:2 * q4]), dec(buf[2 * q4:3 * q4]), dec(buf[3 * q4:])
+    if grpb:
+        d = defaultdict(list)
+        for (c0, t0), (c1, t1) in zip(grpb, grpb[1:]):
+            d[(c0, c1)].append(t1 - t0)
+        for k in sorted(d, key=lambda k: -sum(d[k])):
+            v = np.array(d[k])
+            print(f"  group B {NAMES.get(k[0], k[0]):>12} -> {NAMES.get(k[1], k[1]):<12} n={len(v):4d} median={np.median(v) / 1e3:6.2f}us total={v.sum() / 1e3 / ticks:8.1f}us/tick")
     L = len(widths) - 1
     print(f"== {widths[0]}x{L} M={M} learn={learn} counts={counts}: {ms * 1e3 / ticks:.1f} us/tick")
     dur = defaultdict(list)

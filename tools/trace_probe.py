@@ -61,6 +61,10 @@ def run(widths, D, learn=True, ticks=8, cta=0):
 
 if __name__ == "__main__":
     which = sys.argv[1] if len(sys.argv) > 1 else "all"
+    if which == "small":
+        run([2048] * 5, 1, ticks=16)
+        run([2048] * 5, 1, ticks=16, learn=False)
+        sys.exit(0)
     run([2048] * 33, 1)
     if which == "all":
         run([2048] * 33, 1, cta=100)
