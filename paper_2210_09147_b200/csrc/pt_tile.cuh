@@ -304,8 +304,9 @@ __device__ void t_mma(const TParams& P, const TSmem& sm, uint32_t tbase) {
             const int slot = j % T_NSLOT, b = j & 1;
             const float* hi = sm.ring + size_t(slot) * T_SLOT_FLOATS;
             const float* opn = sm.opnd + size_t(b) * 2 * M * T_CK;
-            t_wait(&sm.prep[b], (j >> 1) & 1, P);  // operands and the lo tile
+            t_wait(&sm.opnd_rdy[b], (j >> 1) & 1, P);  // operands (group B)
             t_wait(&sm.full[slot], (j / T_NSLOT) & 1, P);
+            t_wait(&sm.prep[b], (j >> 1) & 1, P);  // lo tile in TMEM (group A)
             t_trace(P, tr, 20);
             tc_fence_after();
             // descriptors advance by constants per K-step (start-address field, 16-B units):
@@ -362,7 +363,7 @@ struct TOpnd {
   // k-quads)
   float v[8];
   __device__ __forceinline__ void fetch(const float* src, int ld, int) {
-    const int st = threadIdx.x - T_SIMT0, lane = st & 31, w = st >> 5;
+    const int st = (threadIdx.x - T_SIMT0) & (T_GRP - 1), lane = st & 31, w = st >> 5;
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const int idx = w * 8 + q, m = (idx & 1) * 8 + (lane >> 2), k = (idx >> 1) * 4 + (lane & 3);
@@ -372,7 +373,7 @@ struct TOpnd {
   // dop != nullptr (B chunks): also the update MMA's B operand [delta_hi; delta_lo]^T, rows
   // r (64 hi + 64 lo) x K = m (16), no-swizzle K-major (SBO 512 B)
   __device__ __forceinline__ void put(float* ohi, float* olo, float* dop, int) const {
-    const int st = threadIdx.x - T_SIMT0, lane = st & 31, w = st >> 5;
+    const int st = (threadIdx.x - T_SIMT0) & (T_GRP - 1), lane = st & 31, w = st >> 5;
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const int idx = w * 8 + q, mg = idx & 1, kq = idx >> 1;
@@ -570,51 +571,19 @@ __global__ void __launch_bounds__(T_THREADS, 1) tile_kernel(const __grid_constan
           for (int u = c; u < sp.nunits; u += G, ++uc) {
             const int blk = u / T_Q, q = u % T_Q;
             if (grp == 0) {
-              // ===================== group A: operands, lo tiles, accumulator epilogue
-              if (!sp.fwd && upd) {
-                // A operand of the update MMAs: a_i^T of the unit's 128 columns (backward
-                // cache), tf32 hi / lo, no-swizzle K-major [128][16]; published with chunk
-                // 0's prep. The previous unit's MMAs are complete (its epilogue waited).
-                const int cbase = blk * 128;
-                for (int e = st_id; e < 128 * T_MAXM; e += T_GRP) {
-                  const int m = e >> 7, cc = e & 127;
-                  const float x = t_ld(Cb + L.a_in + size_t(m) * L.n_in + cbase + cc);
-                  const int o = int(tc_kmajor_noswz_off(cc, m, T_MAXM) >> 2);
-                  const float h = tf32_hi(x);
-                  sm.aop[o] = h;
-                  sm.aop[128 * T_MAXM + o] = x - h;
-                }
-              }
-              // operand source of chunk ch: F = a_i[:, cols], B = delta[:, rows]
-              const float* osrc;
-              int old;
-              if (sp.fwd) {
-                const int c0 = q * (L.n_in / T_Q);
-                osrc = (i == 0) ? in + c0 : Ccur + L.a_in + c0;
-                old = (i == 0) ? ld_in0 : L.n_in;
-              } else {
-                osrc = P.delta + q * (L.n_out / T_Q);
-                old = P.max_n;
-              }
-              TOpnd op;
-              op.fetch(osrc, old, M);
+              // ===================== group A: lo tiles (TMEM), accumulator epilogue
               for (int ch = 0; ch < sp.nchunks; ++ch, ++j) {
                 const int slot = j % T_NSLOT, b = j & 1;
                 const float* tile = sm.ring + size_t(slot) * T_SLOT_FLOATS;
                 const uint32_t lot = tbase + T_LO_COL + uint32_t(b) * T_CK;  // lo tile in TMEM
-                float* ohi = sm.opnd + size_t(b) * 2 * ob;
-                float* dopb = sm.dop + size_t(b) * 2 * T_CK * T_MAXM;
                 t_trace(P, tr, 6);
-                if (j >= 2) t_wait(&sm.mdone[b], ((j - 2) >> 1) & 1, P);  // operand / TMEM buffers free
+                if (j >= 2) t_wait(&sm.mdone[b], ((j - 2) >> 1) & 1, P);  // lo buffer free
                 tc_fence_after();
-                op.put(ohi, ohi + ob, sp.fwd ? nullptr : dopb, M);
-                if (ch + 1 < sp.nchunks) op.fetch(osrc + (ch + 1) * T_CK, old, M);
                 t_wait(&sm.full[slot], (j / T_NSLOT) & 1, P);
                 t_trace(P, tr, 7);
                 if (sp.fwd) t_lo_pass_f(tile, lot);
                 else t_lo_pass_b(tile, lot);
                 t_trace(P, tr, 13);
-                fence_proxy_async_shared();  // operands -> the tensor core (async proxy)
                 tc_fence_before();
                 grp_sync(0);
                 if (st_id == 0) mbar_arrive(&sm.prep[b]);
@@ -639,28 +608,72 @@ __global__ void __launch_bounds__(T_THREADS, 1) tile_kernel(const __grid_constan
               grp_sync(0);
               if (st_id == 0) mbar_arrive(&sm.afree[uc & 1]);
             } else {
-              // ===================== group B: SGD write-back of the backward tiles
-              if (sp.fwd) {
-                j += sp.nchunks;
-              } else {
-                for (int ch = 0; ch < sp.nchunks; ++ch, ++j, ++bj) {
-                  const int slot = j % T_NSLOT, b = j & 1;
-                  t_trace(P, tr, 8);
-                  t_wait(&sm.mdone[b], (j >> 1) & 1, P);
-                  tc_fence_after();
-                  t_trace(P, tr, 9);
-                  if (upd) {
-                    t_apply_update(sm.ring + size_t(slot) * T_SLOT_FLOATS, tbase + T_UPD_COL + (bj & 1) * 128, nlr);
-                    fence_proxy_async_shared();  // W' -> the producer's TMA store
-                  }
-                  tc_fence_before();
-                  grp_sync(1);
-                  if (st_id == T_GRP) {
-                    mbar_arrive(&sm.sfree[slot]);
-                    mbar_arrive(&sm.applied[bj & 1]);
-                  }
-                  t_trace(P, tr, 10);
+              // ===================== group B: operands (smem), SGD write-back of backward tiles
+              const int gst = st_id - T_GRP;
+              if (!sp.fwd && upd) {
+                // A operand of the update MMAs: a_i^T of the unit's 128 columns (backward
+                // cache), tf32 hi / lo, no-swizzle K-major [128][16]; published with chunk
+                // 0's operands. The previous unit's MMAs are complete (its last apply waited).
+                const int cbase = blk * 128;
+                for (int e = gst; e < 128 * T_MAXM; e += T_GRP) {
+                  const int m = e >> 7, cc = e & 127;
+                  const float x = t_ld(Cb + L.a_in + size_t(m) * L.n_in + cbase + cc);
+                  const int o = int(tc_kmajor_noswz_off(cc, m, T_MAXM) >> 2);
+                  const float h = tf32_hi(x);
+                  sm.aop[o] = h;
+                  sm.aop[128 * T_MAXM + o] = x - h;
                 }
+              }
+              // operand source of chunk ch: F = a_i[:, cols], B = delta[:, rows]
+              const float* osrc;
+              int old;
+              if (sp.fwd) {
+                const int c0 = q * (L.n_in / T_Q);
+                osrc = (i == 0) ? in + c0 : Ccur + L.a_in + c0;
+                old = (i == 0) ? ld_in0 : L.n_in;
+              } else {
+                osrc = P.delta + q * (L.n_out / T_Q);
+                old = P.max_n;
+              }
+              TOpnd op;
+              op.fetch(osrc, old, M);
+              auto apply = [&](uint32_t jj, uint32_t bb) {
+                // chunk jj: all its MMAs are done -> SGD step in place -> producer stores the tile
+                const int pslot = jj % T_NSLOT;
+                t_wait(&sm.mdone[jj & 1], (jj >> 1) & 1, P);
+                tc_fence_after();
+                t_trace(P, tr, 9);
+                if (upd) {
+                  t_apply_update(sm.ring + size_t(pslot) * T_SLOT_FLOATS, tbase + T_UPD_COL + (bb & 1) * 128, nlr);
+                  fence_proxy_async_shared();  // W' -> the producer's TMA store
+                }
+                tc_fence_before();
+                grp_sync(1);
+                if (gst == 0) {
+                  mbar_arrive(&sm.sfree[pslot]);
+                  mbar_arrive(&sm.applied[bb & 1]);
+                }
+                t_trace(P, tr, 10);
+              };
+              for (int ch = 0; ch < sp.nchunks; ++ch, ++j) {
+                const int b = j & 1;
+                float* ohi = sm.opnd + size_t(b) * 2 * ob;
+                float* dopb = sm.dop + size_t(b) * 2 * T_CK * T_MAXM;
+                t_trace(P, tr, 8);
+                if (j >= 2) t_wait(&sm.mdone[b], ((j - 2) >> 1) & 1, P);  // operand buffers free
+                op.put(ohi, ohi + ob, sp.fwd ? nullptr : dopb, M);
+                if (ch + 1 < sp.nchunks) op.fetch(osrc + (ch + 1) * T_CK, old, M);
+                fence_proxy_async_shared();  // operands -> the tensor core (async proxy)
+                grp_sync(1);
+                if (gst == 0) mbar_arrive(&sm.opnd_rdy[b]);
+                if (!sp.fwd) {
+                  if (ch > 0) apply(j - 1, bj);
+                  if (ch > 0) ++bj;
+                }
+              }
+              if (!sp.fwd) {
+                apply(j - 1, bj);
+                ++bj;
               }
             }
           }
