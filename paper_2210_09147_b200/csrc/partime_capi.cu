@@ -459,8 +459,8 @@ int setup_tile(pt_pipeline* p) {
   CUDA_TRY(cudaMemcpy(p->d_tlayers, tl.data(), tl.size() * sizeof(pt::TLayer), cudaMemcpyHostToDevice));
   CUDA_TRY(cudaMemcpy(p->d_tstages, ts.data(), ts.size() * sizeof(pt::TStage), cudaMemcpyHostToDevice));
   // shared memory: 1 KB alignment slack, ring, lo, operands, delta tile, reductions, barriers
-  p->t_smem = 1024 + pt::T_NSLOT * pt::T_SLOT_FLOATS * 4 + 2 * 2 * M * pt::T_CK * 4 + 2 * 2 * pt::T_CK * pt::T_MAXM * 4 + 2 * 128 * pt::T_MAXM * 4 + 64 +
-              (2 * pt::T_NSLOT + 10) * 8 + 16;
+  p->t_smem = 1024 + pt::T_NSLOT * pt::T_SLOT_FLOATS * 4 + pt::T_NB * 2 * M * pt::T_CK * 4 + pt::T_NB * 2 * pt::T_CK * pt::T_MAXM * 4 + 2 * 128 * pt::T_MAXM * 4 + 64 +
+              (3 * pt::T_NSLOT + 5 * pt::T_NB + 4) * 8 + 16;
   if (p->t_smem > pt::SMEM_MAX) return fail(PT_EINVAL, "tile path shared-memory plan exceeds 227 KB");
   CUDA_TRY(cudaFuncSetAttribute(pt::tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, p->t_smem));
   return PT_OK;

@@ -35,6 +35,7 @@ constexpr int T_THREADS = 320;
 constexpr int T_SIMT0 = 64;            // first SIMT thread
 constexpr int T_NS = 256;              // SIMT threads
 constexpr int T_NSLOT = 5;             // weight ring slots of 32 KB
+constexpr int T_NB = 3;                // operand / lo-tile buffers (chunks in flight between SIMT and MMA)
 constexpr int T_SLOT_FLOATS = 8192;
 constexpr int T_CK = 64;               // F: chunk columns; B: chunk rows
 constexpr int T_Q = 4;                 // quarters (columns in F, rows in B)
@@ -43,7 +44,7 @@ constexpr int T_NACC = 1;              // independent accumulators per unit (K-s
 constexpr int T_ACC_COLS = 2 * T_NACC * 32;  // TMEM columns of the two unit accumulators
 constexpr int T_TMEM_COLS = 512;        // accumulators, two 64-column lo tiles, two 128-column update tiles
 constexpr int T_LO_COL = T_ACC_COLS;    // lo tiles (A operand of the lo MMAs)
-constexpr int T_UPD_COL = T_ACC_COLS + 2 * T_CK;  // update products D[c][r] (B steps)
+constexpr int T_UPD_COL = T_ACC_COLS + T_NB * T_CK;  // update products D[c][r] (B steps)
 static_assert(T_UPD_COL + 2 * 128 <= T_TMEM_COLS, "TMEM plan exceeds the allocation");
 constexpr int T_DTS = 24;              // dT row stride (floats): conflict-free staging, 16-B rows
 
@@ -184,9 +185,11 @@ struct TSmem {
   float* aop;       // B: update MMA A operand a^T (hi, lo) of the unit's 128 columns, [2][128][16]
   float* red;       // 16 floats
   uint64_t* full;   // [T_NSLOT]
-  uint64_t* sfree;  // [T_NSLOT] slot consumed (F: MMAs done; B: update done)
+  uint64_t* sfree;  // [T_NSLOT] forward chunk in the slot consumed (MMA commit)
+  uint64_t* bfree;  // [T_NSLOT] backward chunk in the slot updated in place (4 write-back warps)
   uint64_t* opnd_rdy; // [2] operand chunk staged
-  uint64_t* prep;   // [2] lo tile written (and, in B, the updated weights computed)
+  uint64_t* prep;   // [T_NB] lo tile written (group A; the whole tile in B, K half 0 in F)
+  uint64_t* prep2;  // [T_NB] forward chunks: K half 1 of the lo tile written (group B)
   uint64_t* mhi;    // [2] hi MMAs of the chunk done (raw tile no longer read)
   uint64_t* mdone;  // [2] all MMAs of the chunk done
   uint64_t* afree;  // [2] accumulator read by the epilogue
@@ -198,16 +201,28 @@ struct TSmem {
 __device__ void t_producer(const TParams& P, const TSmem& sm) {
   const int c = blockIdx.x, G = P.G;
   uint32_t j = 0;
-  // pending write-backs: slot -> (layer, row, col) of the tile, valid flag
+  // per slot: kind of the chunk it holds (1 forward: released by the MMA commit on sfree,
+  // 2 backward: released by the 4 write-back warps on bfree), completions consumed, and a
+  // pending write-back (layer, row, col) of an updated backward tile
+  int kind[T_NSLOT];
+  uint32_t fcnt[T_NSLOT], bcnt[T_NSLOT];
   int pend_l[T_NSLOT], pend_r[T_NSLOT], pend_c[T_NSLOT];
-  uint32_t pend_j[T_NSLOT];
   bool pend[T_NSLOT];
-  for (int s = 0; s < T_NSLOT; ++s) pend[s] = false;
+  for (int s = 0; s < T_NSLOT; ++s) {
+    pend[s] = false;
+    kind[s] = 0;
+    fcnt[s] = bcnt[s] = 0;
+  }
   bool dead = false;
   int tr = 0;
+  auto release = [&](int s) {
+    if (kind[s] == 1) t_wait(&sm.sfree[s], fcnt[s]++ & 1, P);
+    else if (kind[s] == 2) t_wait(&sm.bfree[s], bcnt[s]++ & 1, P);
+    kind[s] = 0;
+  };
   auto flush = [&](int s) {
     if (!pend[s]) return;
-    t_wait(&sm.sfree[s], (pend_j[s] / T_NSLOT) & 1, P);
+    release(s);
     const CUtensorMap* tm = P.layers[pend_l[s]].tmb;
     float* base = sm.ring + size_t(s) * T_SLOT_FLOATS;
     for (int b = 0; b < 4; ++b) tma_store_2d(tm, base + b * 2048, pend_c[s] + 32 * b, pend_r[s]);
@@ -236,15 +251,14 @@ __device__ void t_producer(const TParams& P, const TSmem& sm) {
           const int blk = u / T_Q, q = u % T_Q;
           for (int ch = 0; ch < sp.nchunks; ++ch, ++j) {
             const int slot = j % T_NSLOT;
-            if (j >= T_NSLOT) {
-              if (pend[slot]) {
-                flush(slot);
-                bulk_commit();
-                bulk_wait_read_all();
-              } else {
-                t_wait(&sm.sfree[slot], ((j - T_NSLOT) / T_NSLOT) & 1, P);
-              }
+            if (pend[slot]) {
+              flush(slot);
+              bulk_commit();
+              bulk_wait_read_all();
+            } else {
+              release(slot);
             }
+            kind[slot] = sp.fwd ? 1 : 2;
             float* dst = sm.ring + size_t(slot) * T_SLOT_FLOATS;
             t_trace(P, tr, 30);
             mbar_arrive_expect_tx(&sm.full[slot], T_SLOT_FLOATS * 4);
@@ -260,7 +274,6 @@ __device__ void t_producer(const TParams& P, const TSmem& sm) {
                 pend_l[slot] = sp.L;
                 pend_r[slot] = r0;
                 pend_c[slot] = c0;
-                pend_j[slot] = j;
               }
             }
             if (ld_volatile_s32(P.status) != ST_OK) dead = true;
@@ -286,7 +299,7 @@ __device__ void t_mma(const TParams& P, const TSmem& sm, uint32_t tbase) {
   // The hi MMAs read the raw TMA tile (the tensor core uses its top 19 bits = tf32(w)),
   // so they start as soon as the tile lands; the lo MMAs wait for the SIMT split.
   const int c = blockIdx.x, G = P.G, M = P.M;
-  uint32_t j = 0, uc = 0, bj = 0;  // chunk, unit, backward-chunk counters
+  uint32_t j = 0, uc = 0, bj = 0, fj = 0;  // chunk, unit, backward-chunk, forward-chunk counters
   int tr = 0;
   for (int ti = 0; ti < P.n; ++ti) {
     for (int s = 0; s < P.n_stages; ++s) {
@@ -301,12 +314,16 @@ __device__ void t_mma(const TParams& P, const TSmem& sm, uint32_t tbase) {
           const uint32_t acc = tbase + (uc & 1) * uint32_t(T_NACC * 2 * M);
           if (uc >= 2) t_wait(&sm.afree[uc & 1], ((uc - 2) >> 1) & 1, P);
           for (int ch = 0; ch < sp.nchunks; ++ch, ++j) {
-            const int slot = j % T_NSLOT, b = j & 1;
+            const int slot = j % T_NSLOT, b = j % T_NB;
             const float* hi = sm.ring + size_t(slot) * T_SLOT_FLOATS;
             const float* opn = sm.opnd + size_t(b) * 2 * M * T_CK;
-            t_wait(&sm.opnd_rdy[b], (j >> 1) & 1, P);  // operands (group B)
+            t_wait(&sm.opnd_rdy[b], (j / T_NB) & 1, P);  // operands (group B)
             t_wait(&sm.full[slot], (j / T_NSLOT) & 1, P);
-            t_wait(&sm.prep[b], (j >> 1) & 1, P);  // lo tile in TMEM (group A)
+            t_wait(&sm.prep[b], (j / T_NB) & 1, P);  // lo tile in TMEM (group A)
+            if (sp.fwd) {
+              t_wait(&sm.prep2[fj % T_NB], (fj / T_NB) & 1, P);  // its second K half (group B)
+              ++fj;
+            }
             t_trace(P, tr, 20);
             tc_fence_after();
             // descriptors advance by constants per K-step (start-address field, 16-B units):
@@ -396,11 +413,10 @@ struct TOpnd {
 // owns TMEM lanes 32 * (warp % 4) .. +31 and both 32-deep K halves of the 64-deep chunk.
 //
 // F chunk (K-major SWIZZLE_128B tile, 2 boxes [128 rows][32 cols]): thread = W row r.
-__device__ __forceinline__ void t_lo_pass_f(const float* tile, uint32_t lo_tmem) {
+__device__ __forceinline__ void t_lo_pass_f(const float* tile, uint32_t lo_tmem, int kh0, int kh1) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = 32 * (warp & 3) + lane;
-#pragma unroll
-  for (int kh = 0; kh < 2; ++kh) {
+  for (int kh = kh0; kh < kh1; ++kh) {
     const float* row = tile + kh * 4096 + r * 32;
     float v[32];
 #pragma unroll
@@ -477,31 +493,39 @@ __global__ void __launch_bounds__(T_THREADS, 1) tile_kernel(const __grid_constan
   const int ob = M * T_CK;
   sm.ring = reinterpret_cast<float*>(base);
   sm.opnd = sm.ring + T_NSLOT * T_SLOT_FLOATS;
-  sm.dop = sm.opnd + 2 * 2 * ob;
-  sm.aop = sm.dop + 2 * 2 * T_CK * T_MAXM;
+  sm.dop = sm.opnd + T_NB * 2 * ob;
+  sm.aop = sm.dop + T_NB * 2 * T_CK * T_MAXM;
   sm.red = sm.aop + 2 * 128 * T_MAXM;
   sm.full = reinterpret_cast<uint64_t*>(sm.red + 16);
   sm.sfree = sm.full + T_NSLOT;
-  sm.opnd_rdy = sm.sfree + T_NSLOT;
-  sm.prep = sm.opnd_rdy + 2;
-  sm.mhi = sm.prep + 2;
-  sm.mdone = sm.mhi + 2;
-  sm.afree = sm.mdone + 2;
+  sm.bfree = sm.sfree + T_NSLOT;
+  sm.opnd_rdy = sm.bfree + T_NSLOT;
+  sm.prep = sm.opnd_rdy + T_NB;
+  sm.prep2 = sm.prep + T_NB;
+  sm.mhi = sm.prep2 + T_NB;
+  sm.mdone = sm.mhi + T_NB;
+  sm.afree = sm.mdone + T_NB;
   sm.applied = sm.afree + 2;
   sm.tmem = reinterpret_cast<uint32_t*>(sm.applied + 2);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
+    // barriers arrived by a SIMT group count its 4 warps (one arrival per warp, no group
+    // barrier needed); tensor-core commits and the producer arrive once
     for (int s = 0; s < T_NSLOT; ++s) {
       mbar_init(&sm.full[s], 1);
       mbar_init(&sm.sfree[s], 1);
+      mbar_init(&sm.bfree[s], 4);
+    }
+    for (int b = 0; b < T_NB; ++b) {
+      mbar_init(&sm.opnd_rdy[b], 4);
+      mbar_init(&sm.mhi[b], 1);
+      mbar_init(&sm.prep[b], 4);
+      mbar_init(&sm.prep2[b], 4);
+      mbar_init(&sm.mdone[b], 1);
     }
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&sm.opnd_rdy[b], 1);
-      mbar_init(&sm.mhi[b], 1);
-      mbar_init(&sm.prep[b], 1);
-      mbar_init(&sm.mdone[b], 1);
-      mbar_init(&sm.afree[b], 1);
-      mbar_init(&sm.applied[b], 1);
+      mbar_init(&sm.afree[b], 4);
+      mbar_init(&sm.applied[b], 4);
     }
     fence_mbar_init();
   }
@@ -521,7 +545,7 @@ __global__ void __launch_bounds__(T_THREADS, 1) tile_kernel(const __grid_constan
     const int gtid = c * T_NS + st_id, gthreads = G * T_NS;
     const float nlr = -P.lr;
     const float inv_mf = 1.f / float(M * P.F);
-    uint32_t j = 0, uc = 0, bj = 0;
+    uint32_t j = 0, uc = 0, bj = 0, fj = 0;
     u64 gen = 0;
     int tr = 0;
     for (int ti = 0; ti < P.n; ++ti) {
@@ -573,24 +597,24 @@ __global__ void __launch_bounds__(T_THREADS, 1) tile_kernel(const __grid_constan
             if (grp == 0) {
               // ===================== group A: lo tiles (TMEM), accumulator epilogue
               for (int ch = 0; ch < sp.nchunks; ++ch, ++j) {
-                const int slot = j % T_NSLOT, b = j & 1;
+                const int slot = j % T_NSLOT, b = j % T_NB;
                 const float* tile = sm.ring + size_t(slot) * T_SLOT_FLOATS;
                 const uint32_t lot = tbase + T_LO_COL + uint32_t(b) * T_CK;  // lo tile in TMEM
                 t_trace(P, tr, 6);
-                if (j >= 2) t_wait(&sm.mdone[b], ((j - 2) >> 1) & 1, P);  // lo buffer free
+                if (j >= T_NB) t_wait(&sm.mdone[b], ((j - T_NB) / T_NB) & 1, P);  // lo buffer free
                 tc_fence_after();
                 t_wait(&sm.full[slot], (j / T_NSLOT) & 1, P);
                 t_trace(P, tr, 7);
-                if (sp.fwd) t_lo_pass_f(tile, lot);
+                if (sp.fwd) t_lo_pass_f(tile, lot, 0, 1);
                 else t_lo_pass_b(tile, lot);
                 t_trace(P, tr, 13);
                 tc_fence_before();
-                grp_sync(0);
-                if (st_id == 0) mbar_arrive(&sm.prep[b]);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&sm.prep[b]);
               }
               // unit epilogue: last chunk's MMAs complete -> accumulator -> quarter partials
               const uint32_t jl = j - 1;
-              t_wait(&sm.mdone[jl & 1], (jl >> 1) & 1, P);
+              t_wait(&sm.mdone[jl % T_NB], (jl / T_NB) & 1, P);
               tc_fence_after();
               {
                 const int lq = warp & 3;
@@ -605,8 +629,8 @@ __global__ void __launch_bounds__(T_THREADS, 1) tile_kernel(const __grid_constan
                 for (int m = 0; m < 16; ++m) dst[size_t(m) * P.max_n] = v[m];
               }
               tc_fence_before();
-              grp_sync(0);
-              if (st_id == 0) mbar_arrive(&sm.afree[uc & 1]);
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&sm.afree[uc & 1]);
             } else {
               // ===================== group B: operands (smem), SGD write-back of backward tiles
               const int gst = st_id - T_GRP;
@@ -640,7 +664,7 @@ __global__ void __launch_bounds__(T_THREADS, 1) tile_kernel(const __grid_constan
               auto apply = [&](uint32_t jj, uint32_t bb) {
                 // chunk jj: all its MMAs are done -> SGD step in place -> producer stores the tile
                 const int pslot = jj % T_NSLOT;
-                t_wait(&sm.mdone[jj & 1], (jj >> 1) & 1, P);
+                t_wait(&sm.mdone[jj % T_NB], (jj / T_NB) & 1, P);
                 tc_fence_after();
                 t_trace(P, tr, 9);
                 if (upd) {
@@ -648,24 +672,36 @@ __global__ void __launch_bounds__(T_THREADS, 1) tile_kernel(const __grid_constan
                   fence_proxy_async_shared();  // W' -> the producer's TMA store
                 }
                 tc_fence_before();
-                grp_sync(1);
-                if (gst == 0) {
-                  mbar_arrive(&sm.sfree[pslot]);
+                __syncwarp();
+                if (lane == 0) {
+                  mbar_arrive(&sm.bfree[pslot]);
                   mbar_arrive(&sm.applied[bb & 1]);
                 }
                 t_trace(P, tr, 10);
               };
               for (int ch = 0; ch < sp.nchunks; ++ch, ++j) {
-                const int b = j & 1;
+                const int b = j % T_NB;
                 float* ohi = sm.opnd + size_t(b) * 2 * ob;
                 float* dopb = sm.dop + size_t(b) * 2 * T_CK * T_MAXM;
                 t_trace(P, tr, 8);
-                if (j >= 2) t_wait(&sm.mdone[b], ((j - 2) >> 1) & 1, P);  // operand buffers free
+                if (j >= T_NB) t_wait(&sm.mdone[b], ((j - T_NB) / T_NB) & 1, P);  // operand buffers free
+                tc_fence_after();
                 op.put(ohi, ohi + ob, sp.fwd ? nullptr : dopb, M);
                 if (ch + 1 < sp.nchunks) op.fetch(osrc + (ch + 1) * T_CK, old, M);
                 fence_proxy_async_shared();  // operands -> the tensor core (async proxy)
-                grp_sync(1);
-                if (gst == 0) mbar_arrive(&sm.opnd_rdy[b]);
+                if (sp.fwd) {
+                  // forward: group B also writes K half 1 of the lo tile
+                  const int slot = j % T_NSLOT;
+                  t_wait(&sm.full[slot], (j / T_NSLOT) & 1, P);
+                  t_lo_pass_f(sm.ring + size_t(slot) * T_SLOT_FLOATS, tbase + T_LO_COL + uint32_t(b) * T_CK, 1, 2);
+                  tc_fence_before();
+                }
+                __syncwarp();
+                if (lane == 0) {
+                  mbar_arrive(&sm.opnd_rdy[b]);
+                  if (sp.fwd) mbar_arrive(&sm.prep2[fj % T_NB]);
+                }
+                if (sp.fwd) ++fj;
                 if (!sp.fwd) {
                   if (ch > 0) apply(j - 1, bj);
                   if (ch > 0) ++bj;

@@ -58,6 +58,14 @@ def run(widths, counts, ticks=2, M=16, learn=True, cta=0):
     if prod:
         t = np.array([x for _, x in prod])
         print(f"  producer: {len(t)} loads, median gap {np.median(np.diff(t)) / 1e3:.2f}us")
+        fs = [x for c_, x in cons if c_ == 7]
+        n = min(len(fs), len(t))
+        lat = np.array(fs[:n]) - t[:n]
+        print(f"  TMA issue -> group A sees full: median {np.median(lat) / 1e3:.2f}us p10 {np.percentile(lat, 10) / 1e3:.2f} p90 {np.percentile(lat, 90) / 1e3:.2f}")
+        mp = [x for c_, x in mma if c_ == 20]
+        n2 = min(len(mp), len(t))
+        lat2 = np.array(mp[:n2]) - t[:n2]
+        print(f"  TMA issue -> MMA starts chunk: median {np.median(lat2) / 1e3:.2f}us")
     base = cons[0][1]
     print("  first SIMT events:", [(NAMES.get(c, c), round((x - base) / 1e3, 2)) for c, x in cons[:60]])
     p.close()
