@@ -76,6 +76,25 @@ struct CommLayout {
   size_t gslot(int p) const { return DATA + 2 * inslot_bytes + size_t(p) * gslot_bytes; }
 };
 
+// Tile-path comm block of one stage: four counters on separate 128-B lines, then plain
+// fp32 slots inslot[2][M][n0] and gslot[2][M][nk]. Counters (ticks, monotonic):
+// IN_READY  inslot writes published by the upstream stage;
+// G_READY   gslot writes published by the downstream stage;
+// ACT_CREDIT ticks whose inslot the downstream stage has finished reading (upstream's block);
+// G_CREDIT   ticks whose gslot the upstream stage has finished reading (downstream's block).
+struct TileComm {
+  static constexpr size_t IN_READY = 0, G_READY = 128, ACT_CREDIT = 256, G_CREDIT = 384, DATA = 512;
+  size_t in_bytes = 0, g_bytes = 0, total = 0;
+  TileComm() = default;
+  TileComm(int M, int n0, int nk) {
+    in_bytes = align_up(size_t(M) * n0 * 4, 256);
+    g_bytes = align_up(size_t(M) * nk * 4, 256);
+    total = DATA + 2 * in_bytes + 2 * g_bytes;
+  }
+  size_t inslot(int j) const { return DATA + size_t(j) * in_bytes; }
+  size_t gslot(int j) const { return DATA + 2 * in_bytes + size_t(j) * g_bytes; }
+};
+
 struct IpcBlob {
   int32_t magic, abi, stage, G, M, ld0, ldk, pad_;
   int64_t comm_bytes;
@@ -108,8 +127,9 @@ struct StageHost {
   // micro-batch tile path (plain fp32 buffers): cache[2] slots of a_0..a_k, inslot[2], gslot[2]
   float* tcache = nullptr;
   size_t tcache_floats = 0;
-  float* tin = nullptr;  // [2][M][n0]
-  float* tg = nullptr;   // [2][M][nk]
+  char* tcomm = nullptr;  // tile comm block (TileComm layout), exported over CUDA IPC
+  char* tup = nullptr;    // upstream / downstream stages' tile comm blocks (local or IPC-mapped)
+  char* tdown = nullptr;
   int n0 = 0, nk = 0;
 };
 
@@ -169,6 +189,7 @@ struct pt_pipeline {
   CUtensorMap* d_tmaps = nullptr;
   pt::TLayer* d_tlayers = nullptr;
   pt::TStage* d_tstages = nullptr;
+  std::vector<pt::TLayer> t_layers_host;
   int policy = 0;                                     // weight-load L2 hint (env PT_POLICY)
 
   bool has_first() const { return local_first == 0; }
@@ -177,6 +198,7 @@ struct pt_pipeline {
   int stage_ld0(int s0) const { return pad_dim(dims[sfl[s0]]); }      // s0: 0-based stage
   int stage_ldk(int s0) const { return pad_dim(dims[sfl[s0 + 1]]); }
   CommLayout layout_of(int s0) const { return CommLayout(M, stage_ld0(s0), stage_ldk(s0)); }
+  TileComm tile_layout_of(int s0) const { return TileComm(M, dims[sfl[s0]], dims[sfl[s0 + 1]]); }
 };
 
 namespace {
@@ -393,6 +415,50 @@ int plan_smem(pt_pipeline* p) {
   return PT_OK;
 }
 
+// Stage descriptors of the tile path (rebuilt after every IPC import).
+int upload_tile_stages(pt_pipeline* p) {
+  const int M = p->M;
+  std::vector<pt::TStage> ts(p->stages.size());
+  for (size_t s = 0; s < p->stages.size(); ++s) {
+    const StageHost& S = p->stages[s];
+    const int s0 = S.h - 1;
+    pt::TStage& d = ts[s];
+    memset(&d, 0, sizeof(d));
+    d.h = S.h;
+    d.first = S.first_local;
+    d.k = S.k;
+    d.n0 = S.n0;
+    d.nk = S.nk;
+    const TileComm own = p->tile_layout_of(s0);
+    for (int j = 0; j < 2; ++j) {
+      d.cache[j] = S.tcache + size_t(j) * S.tcache_floats;
+      d.inslot[j] = reinterpret_cast<float*>(S.tcomm + own.inslot(j));
+      d.gslot[j] = reinterpret_cast<float*>(S.tcomm + own.gslot(j));
+    }
+    d.in_ready = reinterpret_cast<u64*>(S.tcomm + TileComm::IN_READY);
+    d.g_ready = reinterpret_cast<u64*>(S.tcomm + TileComm::G_READY);
+    d.act_credit = reinterpret_cast<u64*>(S.tcomm + TileComm::ACT_CREDIT);
+    d.g_credit = reinterpret_cast<u64*>(S.tcomm + TileComm::G_CREDIT);
+    if (S.tdown) {
+      const TileComm dn = p->tile_layout_of(s0 + 1);
+      for (int j = 0; j < 2; ++j) d.down_inslot[j] = reinterpret_cast<float*>(S.tdown + dn.inslot(j));
+      d.peer_in_ready = reinterpret_cast<u64*>(S.tdown + TileComm::IN_READY);
+      d.peer_g_credit = reinterpret_cast<u64*>(S.tdown + TileComm::G_CREDIT);
+      d.down_remote = S.down_remote ? 1 : 0;
+    }
+    if (S.tup) {
+      const TileComm upl = p->tile_layout_of(s0 - 1);
+      for (int j = 0; j < 2; ++j) d.up_gslot[j] = reinterpret_cast<float*>(S.tup + upl.gslot(j));
+      d.peer_g_ready = reinterpret_cast<u64*>(S.tup + TileComm::G_READY);
+      d.peer_act_credit = reinterpret_cast<u64*>(S.tup + TileComm::ACT_CREDIT);
+      d.up_remote = S.up_remote ? 1 : 0;
+    }
+    (void)M;
+  }
+  CUDA_TRY(cudaMemcpy(p->d_tstages, ts.data(), ts.size() * sizeof(pt::TStage), cudaMemcpyHostToDevice));
+  return PT_OK;
+}
+
 // Buffers, tensor maps and descriptors of the micro-batch tile path (pt_tile.cuh).
 int setup_tile(pt_pipeline* p) {
   const int M = p->M;
@@ -418,7 +484,6 @@ int setup_tile(pt_pipeline* p) {
     tl[i].n_out = Lh.n_out;
     tl[i].act = Lh.act;
   }
-  std::vector<pt::TStage> ts(p->stages.size());
   for (size_t s = 0; s < p->stages.size(); ++s) {
     StageHost& S = p->stages[s];
     S.n0 = p->dims[S.first_global];
@@ -433,31 +498,19 @@ int setup_tile(pt_pipeline* p) {
     off += size_t(M) * S.nk;
     S.tcache_floats = align_up(off, 64);
     PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&S.tcache), 2 * S.tcache_floats * 4));
-    PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&S.tin), 2 * size_t(M) * S.n0 * 4));
-    PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&S.tg), 2 * size_t(M) * S.nk * 4));
+    PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&S.tcomm), p->tile_layout_of(S.h - 1).total));
   }
+  // local neighbours
   for (size_t s = 0; s < p->stages.size(); ++s) {
-    StageHost& S = p->stages[s];
-    pt::TStage& d = ts[s];
-    memset(&d, 0, sizeof(d));
-    d.h = S.h;
-    d.first = S.first_local;
-    d.k = S.k;
-    d.n0 = S.n0;
-    d.nk = S.nk;
-    for (int j = 0; j < 2; ++j) {
-      d.cache[j] = S.tcache + size_t(j) * S.tcache_floats;
-      d.inslot[j] = S.tin + size_t(j) * M * S.n0;
-      d.gslot[j] = S.tg + size_t(j) * M * S.nk;
-      if (s + 1 < p->stages.size()) d.down_inslot[j] = p->stages[s + 1].tin + size_t(j) * M * p->stages[s + 1].n0;
-      if (s > 0) d.up_gslot[j] = p->stages[s - 1].tg + size_t(j) * M * p->stages[s - 1].nk;
-    }
+    if (s > 0) p->stages[s].tup = p->stages[s - 1].tcomm;
+    if (s + 1 < p->stages.size()) p->stages[s].tdown = p->stages[s + 1].tcomm;
   }
   PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&p->d_tlayers), tl.size() * sizeof(pt::TLayer)));
-  PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&p->d_tstages), ts.size() * sizeof(pt::TStage)));
+  PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&p->d_tstages), p->stages.size() * sizeof(pt::TStage)));
   CUDA_TRY(cudaMemcpy(p->d_tmaps, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
   CUDA_TRY(cudaMemcpy(p->d_tlayers, tl.data(), tl.size() * sizeof(pt::TLayer), cudaMemcpyHostToDevice));
-  CUDA_TRY(cudaMemcpy(p->d_tstages, ts.data(), ts.size() * sizeof(pt::TStage), cudaMemcpyHostToDevice));
+  p->t_layers_host = tl;
+  PT_TRY(upload_tile_stages(p));
   // shared memory: 1 KB alignment slack, ring, lo, operands, delta tile, reductions, barriers
   p->t_smem = 1024 + pt::T_NSLOT * pt::T_SLOT_FLOATS * 4 + pt::T_NB * 2 * M * pt::T_CK * 4 + pt::T_NB * 2 * pt::T_CK * pt::T_MAXM * 4 + 2 * 128 * pt::T_MAXM * 4 + 64 +
               (3 * pt::T_NSLOT + 5 * pt::T_NB + 4) * 8 + 16;
@@ -510,14 +563,14 @@ int create_impl(const pt_config* c, pt_pipeline* p) {
   if (p->G > sms * per_sm) return fail(PT_EINVAL, "grid exceeds co-resident CTA capacity");
   {
     // micro-batch tensor-core path: every width a multiple of 256, M == 16, all stages here
-    bool ok = p->M == 16 && p->local_count == p->D && p->opt == PT_OPT_SGD && p->loss == PT_LOSS_MSE;
+    bool ok = p->M == 16 && p->opt == PT_OPT_SGD && p->loss == PT_LOSS_MSE;
     int units = 0;
     for (int i = 0; i <= p->L && ok; ++i) ok = (p->dims[i] % 256) == 0;
     for (int i = 0; i < p->L && ok; ++i) units = std::max(units, std::max(p->dims[i + 1], p->dims[i]) / 128 * pt::T_Q);
     if (const char* e = getenv("PT_TILE")) ok = ok && atoi(e) != 0;
-    if (ok && c->grid <= 0) {
+    if (ok) {
       p->tile = true;
-      p->G = std::min(sms, units);
+      p->G = std::min(c->grid > 0 ? c->grid : sms, units);
     }
   }
 
@@ -618,6 +671,11 @@ LayerHost* local_layer(pt_pipeline* p, int layer, std::string* why) {
 int check_ready(pt_pipeline* p) {
   if (p->broken) return fail(PT_ESTATE, "pipeline unusable after an earlier device-side failure");
   for (const StageHost& S : p->stages) {
+    if (p->tile) {
+      if ((S.h > 1 && !S.tup) || (S.h < p->D && !S.tdown))
+        return fail(PT_EINVAL, "stage " + std::to_string(S.h) + ": neighbour stage not imported (pt_ipc_import)");
+      continue;
+    }
     if (S.h > 1 && !S.up)
       return fail(PT_EINVAL, "stage " + std::to_string(S.h) + ": upstream stage not imported (pt_ipc_import)");
     if (S.h < p->D && !S.down)
@@ -997,10 +1055,11 @@ int pt_ipc_export(pt_pipeline* p, int32_t stage, void* buf, size_t cap, size_t* 
   b.M = p->M;
   b.ld0 = S.ld0;
   b.ldk = S.ldk;
-  b.comm_bytes = int64_t(p->layout_of(stage - 1).total);
+  char* block = p->tile ? S.tcomm : S.comm;
+  b.comm_bytes = int64_t(p->tile ? p->tile_layout_of(stage - 1).total : p->layout_of(stage - 1).total);
   b.pid = int64_t(getpid());
-  b.dev_ptr = uint64_t(reinterpret_cast<uintptr_t>(S.comm));
-  CUDA_TRY(cudaIpcGetMemHandle(&b.handle, S.comm));
+  b.dev_ptr = uint64_t(reinterpret_cast<uintptr_t>(block));
+  CUDA_TRY(cudaIpcGetMemHandle(&b.handle, block));
   memcpy(buf, &b, sizeof(b));
   *len = sizeof(b);
   return PT_OK;
@@ -1015,7 +1074,7 @@ int pt_ipc_import(pt_pipeline* p, const void* buf, size_t len) {
   const int s0 = b.stage - 1;
   if (s0 < 0 || s0 >= p->D) return fail(PT_EINVAL, "IPC blob stage out of range");
   if (b.M != p->M || b.ld0 != p->stage_ld0(s0) || b.ldk != p->stage_ldk(s0) ||
-      b.comm_bytes != int64_t(p->layout_of(s0).total))
+      b.comm_bytes != int64_t(p->tile ? p->tile_layout_of(s0).total : p->layout_of(s0).total))
     return fail(PT_EINVAL, "IPC blob shape does not match this pipeline's config");
   const int lo = p->local_first, hi = p->local_first + p->local_count;  // [lo, hi)
   if (s0 >= lo && s0 < hi) return fail(PT_EINVAL, "stage is local; nothing to import");
@@ -1026,6 +1085,16 @@ int pt_ipc_import(pt_pipeline* p, const void* buf, size_t len) {
   } else {
     CUDA_TRY(cudaIpcOpenMemHandle(&ptr, b.handle, cudaIpcMemLazyEnablePeerAccess));
     p->ipc_opened.push_back(ptr);
+  }
+  if (p->tile) {
+    if (s0 == lo - 1) {
+      p->stages.front().tup = static_cast<char*>(ptr);
+      p->stages.front().up_remote = true;
+    } else {
+      p->stages.back().tdown = static_cast<char*>(ptr);
+      p->stages.back().down_remote = true;
+    }
+    return upload_tile_stages(p);
   }
   if (s0 == lo - 1) {
     p->stages.front().up = static_cast<char*>(ptr);

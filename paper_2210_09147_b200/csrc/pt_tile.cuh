@@ -63,6 +63,17 @@ struct TStage {
   float* gslot[2];       // [M][nk], written by the downstream stage
   float* down_inslot[2]; // downstream stage's inslot (h < D)
   float* up_gslot[2];    // upstream stage's gslot (h > 1)
+  // neighbour in another process (one stage per GPU, CUDA IPC over NVLink): the grid
+  // barriers do not order its accesses, so tick counters do (TileComm in partime_capi.cu)
+  int up_remote, down_remote;
+  u64* in_ready;         // own: inslot ticks published by upstream
+  u64* g_ready;          // own: gslot ticks published by downstream
+  u64* act_credit;       // own: inslot ticks downstream has finished reading
+  u64* g_credit;         // own: gslot ticks upstream has finished reading
+  u64* peer_in_ready;    // downstream's in_ready
+  u64* peer_g_credit;    // downstream's g_credit
+  u64* peer_g_ready;     // upstream's g_ready
+  u64* peer_act_credit;  // upstream's act_credit
 };
 
 struct TParams {
@@ -143,6 +154,19 @@ __device__ __forceinline__ bool t_watch(const TParams& P, uint64_t t_start) {
   }
   return false;
 }
+// one SIMT thread per CTA waits until a (possibly remote) tick counter reaches `target`
+__device__ void t_wait_cnt(const TParams& P, const u64* p, u64 target) {
+  if (threadIdx.x == T_SIMT0 + 0 && target > 0) {
+    if (ld_acquire_sys(p) < target) {
+      const uint64_t t0 = globaltimer();
+      for (unsigned it = 1;; ++it) {
+        if (ld_acquire_sys(p) >= target) break;
+        if ((it & 63u) == 0 && t_watch(P, t0)) break;
+      }
+    }
+  }
+}
+
 __device__ __forceinline__ void t_wait(uint64_t* bar, uint32_t parity, const TParams& P) {
   if (mbar_try_wait(bar, parity)) return;
   const uint64_t t0 = globaltimer();
@@ -568,6 +592,11 @@ __global__ void __launch_bounds__(T_THREADS, 1) tile_kernel(const __grid_constan
           in = S.inslot[prv];
           ld_in0 = S.n0;
         }
+        if (S.up_remote) {
+          // the upstream process has published its tick t-1 activations into inslot
+          t_wait_cnt(P, S.in_ready, u64(t));
+          simt_sync();
+        }
         // private copy of the stage input (inslot is overwritten at t+1 before B reads it)
         for (int e = gtid; e < M * S.n0; e += gthreads) {
           const int m = e / S.n0, k = e - m * S.n0;
@@ -716,6 +745,20 @@ __global__ void __launch_bounds__(T_THREADS, 1) tile_kernel(const __grid_constan
           t_trace(P, tr, 2);
           t_grid_sync(P, gen);
           t_trace(P, tr, 3);
+          // ---------------------------------------------------- cross-process stage exchange
+          const bool last_fwd = sp.fwd && (i == S.k - 1) && h < P.D;   // writes down_inslot, reads gslot
+          const bool first_bwd = !sp.fwd && i == 0 && h > 1;            // writes up_gslot
+          if (sp.fwd && i == 0 && S.up_remote && c == 0 && st_id == 0)
+            red_release_sys(S.peer_act_credit, 1);  // every read of inslot[(t-1)%2] is done
+          if (last_fwd && S.down_remote) {
+            t_wait_cnt(P, S.act_credit, u64(t));          // downstream read what I sent at t-2
+            if (P.learn) t_wait_cnt(P, S.g_ready, u64(t));  // downstream's tick t-1 gradient is in
+            simt_sync();
+          }
+          if (first_bwd && S.up_remote) {
+            t_wait_cnt(P, S.g_credit, u64(t));  // upstream read the gradient I sent at t-2
+            simt_sync();
+          }
           // ---------------------------------------------------- finalize
           if (sp.fwd) {
             const bool last_layer = (i == S.k - 1);
@@ -780,7 +823,15 @@ __global__ void __launch_bounds__(T_THREADS, 1) tile_kernel(const __grid_constan
             }
           }
           t_trace(P, tr, 4);
+          if ((last_fwd && S.down_remote) || (first_bwd && S.up_remote)) __threadfence_system();
           t_grid_sync(P, gen);
+          if (c == 0 && st_id == 0) {
+            if (last_fwd && S.down_remote) {
+              red_release_sys(S.peer_in_ready, 1);                // tick t activations published
+              if (P.learn) red_release_sys(S.peer_g_credit, 1);  // tick t-1 gradient consumed
+            }
+            if (first_bwd && S.up_remote) red_release_sys(S.peer_g_ready, 1);  // tick t gradient published
+          }
           t_trace(P, tr, 5);
         }
       }

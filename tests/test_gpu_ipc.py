@@ -15,25 +15,33 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
-def _stage_pair(widths, counts, lr, xs, ys, grid=74):
+def _sample(xs, M):
+    return xs[0] if M > 1 else xs[0, 0]
+
+
+def _stage_pair(widths, counts, lr, xs, ys, grid=74, M=1):
     from paper_2210_09147_b200 import engine, model as mdl
     m = mdl.mlp(widths, seed=4)
-    a = engine.Pipeline(m, counts, "sgd", lr, xs[0, 0], ys[0, 0], local_stages=(0, 1), grid=grid, timeout_ms=60000)
-    b = engine.Pipeline(m, counts, "sgd", lr, xs[0, 0], ys[0, 0], local_stages=(1, 1), grid=grid, timeout_ms=60000)
+    x0, y0 = _sample(xs, M), _sample(ys, M)
+    a = engine.Pipeline(m, counts, "sgd", lr, x0, y0, local_stages=(0, 1), grid=grid, timeout_ms=60000)
+    b = engine.Pipeline(m, counts, "sgd", lr, x0, y0, local_stages=(1, 1), grid=grid, timeout_ms=60000)
     a.ipc_import(b.ipc_export(2))
     b.ipc_import(a.ipc_export(1))
     return m, a, b
 
 
-@pytest.mark.parametrize("widths,counts,T", [([32, 64, 64, 64, 16], [4, 3], 12),
-                                             ([256, 512, 512, 512, 128], [4, 3], 40)])
-def test_ipc_stage_handles_match_single_handle(widths, counts, T):
+@pytest.mark.parametrize("widths,counts,T,M,grid", [([32, 64, 64, 64, 16], [4, 3], 12, 1, 74),
+                                                    ([256, 512, 512, 512, 128], [4, 3], 40, 1, 74),
+                                                    ([256, 512, 512, 256, 256], [4, 3], 12, 16, 64)])
+def test_ipc_stage_handles_match_single_handle(widths, counts, T, M, grid):
+    """M = 16 with widths % 256 == 0 runs the tcgen05 tile kernel on both handles."""
     import torch
     from paper_2210_09147_b200 import engine, model as mdl, streams
-    st = streams.SmoothStream(widths[0], widths[-1], seed=5)
+    st = streams.SmoothStream(widths[0], widths[-1], seed=5, batch=M)
     xs, ys = st.block(0, T)
     xs, ys = xs.astype(np.float32), ys.astype(np.float32)
-    m, a, b = _stage_pair(widths, counts, 0.05, xs, ys)
+    m, a, b = _stage_pair(widths, counts, 0.05, xs, ys, grid=grid, M=M)
+    assert a.kernel_path == b.kernel_path == ("tile" if M == 16 else "tick")
     sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
     a.set_stream(sa)
     b.set_stream(sb)
@@ -43,7 +51,8 @@ def test_ipc_stage_handles_match_single_handle(widths, counts, T):
     outs, losses, _ = b.run(None, yd, T)
     a.sync()
     b.sync()
-    ref = engine.Pipeline(mdl.mlp(widths, seed=4), counts, "sgd", 0.05, xs[0, 0], ys[0, 0], grid=74)  # same row split
+    ref = engine.Pipeline(mdl.mlp(widths, seed=4), counts, "sgd", 0.05, _sample(xs, M), _sample(ys, M),
+                          grid=grid)  # same work split
     o, l, _ = ref.run(xs, ys)
     assert np.array_equal(outs.cpu().numpy(), o) and np.array_equal(losses.cpu().numpy(), l, equal_nan=True)
     W = [ref.get_layer(j) for j in range(ref.L)]
