@@ -274,3 +274,13 @@ def test_tile_deterministic_and_split():
     assert np.array_equal(res[0][0], res[1][0])
     for (Wa, ba), (Wb, bb) in zip(res[0][1], res[1][1]):
         assert np.array_equal(Wa, Wb) and np.array_equal(ba, bb)
+
+
+def test_tile_non_pow2_widths_d3():
+    """Widths 768 / 1280 (padded row pitch != width) and three stages on one GPU."""
+    _tile_case([256, 768, 1280, 512, 256], [2, 2, 3], 9, 0.02)
+
+
+def test_tile_small_grid():
+    """Fewer CTAs than work units: every CTA walks several units per step."""
+    _tile_case([512, 1024, 512, 256], [2, 3], 6, 0.02, grid=24)
