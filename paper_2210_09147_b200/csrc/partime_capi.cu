@@ -107,6 +107,10 @@ struct LayerHost {
   int n_in = 0, n_out = 0, ld_in = 0, ld_out = 0, act = 0;
   float* W = nullptr;
   float* b = nullptr;
+  float* mW = nullptr;  // Adam state, allocated only for the Adam optimizer
+  float* vW = nullptr;
+  float* mb = nullptr;
+  float* vb = nullptr;
   u64* part[2] = {nullptr, nullptr};
   int rows_per_chunk = 0;
   int cache_in = 0, cache_out = 0;
@@ -195,6 +199,8 @@ struct pt_pipeline {
   bool has_first() const { return local_first == 0; }
   bool has_last() const { return local_first + local_count == D; }
   int F() const { return dims[L]; }
+  // target width: the output vector for MSE, one class index per sample for softmax-CE
+  int Fy() const { return loss == PT_LOSS_SOFTMAX_CE ? 1 : dims[L]; }
   int stage_ld0(int s0) const { return pad_dim(dims[sfl[s0]]); }      // s0: 0-based stage
   int stage_ldk(int s0) const { return pad_dim(dims[sfl[s0 + 1]]); }
   CommLayout layout_of(int s0) const { return CommLayout(M, stage_ld0(s0), stage_ldk(s0)); }
@@ -250,6 +256,10 @@ int upload_desc(pt_pipeline* p) {
     pt::LayerDev& d = ld[i];
     d.W = h.W;
     d.b = h.b;
+    d.mW = h.mW;
+    d.vW = h.vW;
+    d.mb = h.mb;
+    d.vb = h.vb;
     d.part[0] = h.part[0];
     d.part[1] = h.part[1];
     d.n_in = h.n_in;
@@ -522,9 +532,6 @@ int setup_tile(pt_pipeline* p) {
 int create_impl(const pt_config* c, pt_pipeline* p) {
   std::string why;
   if (validate(c, &why) != PT_OK) return fail(PT_EINVAL, why);
-  if (c->loss != PT_LOSS_MSE)
-    return fail(PT_EUNSUPPORTED, "softmax cross-entropy is not implemented on the B200 path");
-  if (c->optimizer != PT_OPT_SGD) return fail(PT_EUNSUPPORTED, "Adam is not implemented on the B200 path");
   p->L = c->n_layers;
   p->D = c->n_stages;
   p->M = c->batch;
@@ -587,6 +594,12 @@ int create_impl(const pt_config* c, pt_pipeline* p) {
     Lh.act = p->act[l];
     PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&Lh.W), size_t(Lh.n_out) * Lh.ld_in * 4));
     PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&Lh.b), size_t(Lh.n_out) * 4));
+    if (p->opt == PT_OPT_ADAM && p->learn) {
+      PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&Lh.mW), size_t(Lh.n_out) * Lh.ld_in * 4));
+      PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&Lh.vW), size_t(Lh.n_out) * Lh.ld_in * 4));
+      PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&Lh.mb), size_t(Lh.n_out) * 4));
+      PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&Lh.vb), size_t(Lh.n_out) * 4));
+    }
     p->layers.push_back(Lh);
   }
   PT_TRY(plan_smem(p));
@@ -644,7 +657,7 @@ int create_impl(const pt_config* c, pt_pipeline* p) {
   const long long big = std::numeric_limits<long long>::max();
   CUDA_TRY(cudaMemcpy(p->d_first_bad, &big, sizeof(big), cudaMemcpyHostToDevice));
   p->yh = std::max(1, p->D);
-  if (p->has_last()) PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&p->yhist), size_t(p->yh) * p->M * p->F() * 4));
+  if (p->has_last()) PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&p->yhist), size_t(p->yh) * p->M * p->Fy() * 4));
   CUDA_TRY(cudaStreamCreateWithFlags(&p->own_stream, cudaStreamNonBlocking));
   p->stream = p->own_stream;
   CUDA_TRY(cudaEventCreate(&p->ev0));
@@ -709,7 +722,7 @@ int run_impl(pt_pipeline* p, const float* xs, const float* ys, int64_t n, float*
   if (where != PT_HOST && where != PT_DEVICE) return fail(PT_EINVAL, "where must be PT_HOST or PT_DEVICE");
   const cudaMemcpyKind h2d = where == PT_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
   const cudaMemcpyKind d2h = where == PT_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
-  const int M = p->M, F = p->F();
+  const int M = p->M, F = p->F(), Fy = p->Fy();
   const bool first = p->has_first(), last = p->has_last();
   if (first && !xs) return fail(PT_EINVAL, "xs is required on the process that owns stage 1");
   if (last && p->learn && !ys) return fail(PT_EINVAL, "targets are required for online learning (stage D)");
@@ -727,8 +740,8 @@ int run_impl(pt_pipeline* p, const float* xs, const float* ys, int64_t n, float*
   if (last) {
     if (ys) {
       if (where == PT_HOST) {
-        PT_TRY(ensure(p, &p->ys_stage, &p->ys_cap, size_t(n), size_t(M) * F));
-        CUDA_TRY(cudaMemcpyAsync(p->ys_stage, ys, size_t(n) * M * F * 4, h2d, p->stream));
+        PT_TRY(ensure(p, &p->ys_stage, &p->ys_cap, size_t(n), size_t(M) * Fy));
+        CUDA_TRY(cudaMemcpyAsync(p->ys_stage, ys, size_t(n) * M * Fy * 4, h2d, p->stream));
         ys_dev = p->ys_stage;
       } else {
         ys_dev = ys;
@@ -770,6 +783,12 @@ int run_impl(pt_pipeline* p, const float* xs, const float* ys, int64_t n, float*
   for (const StageHost& S : p->stages) nB += S.k;
   P.nB = p->learn ? nB : 0;
   P.lr = p->lr;
+  P.loss = p->loss;
+  P.opt = p->opt;
+  P.Fy = Fy;
+  P.b1 = 0.9f;  // Adam (oracle/netcore.py Adam)
+  P.b2 = 0.999f;
+  P.eps = 1e-8f;
   P.xs = first ? p->xs_pad : nullptr;
   P.ys = ys_dev;
   P.yhist = p->yhist;
@@ -858,14 +877,15 @@ int run_impl(pt_pipeline* p, const float* xs, const float* ys, int64_t n, float*
     const int threads = 256, warps_per_block = threads / 32;
     const int blocks = int((n + warps_per_block - 1) / warps_per_block);
     pt::epilogue_kernel<<<blocks, threads, 0, p->stream>>>(p->loss_part, p->G, int(n), p->t_next, p->D,
-                                                           1.f / float(M * F), ys_dev != nullptr ? 1 : 0,
+                                                           p->loss == PT_LOSS_SOFTMAX_CE ? 1.f / float(M) : 1.f / float(M * F),
+                                                           ys_dev != nullptr ? 1 : 0,
                                                            losses_dev, valid_dev, p->d_first_bad);
     CUDA_TRY(cudaGetLastError());
     // queue the last D-1 targets for the next call (target queue)
     if (ys_dev) {
       for (long long s = std::max<long long>(p->t_next, p->t_next + n - (p->D - 1)); s < p->t_next + n; ++s)
-        CUDA_TRY(cudaMemcpyAsync(p->yhist + size_t(s % p->yh) * M * F, ys_dev + size_t(s - p->t_next) * M * F,
-                                 size_t(M) * F * 4, cudaMemcpyDeviceToDevice, p->stream));
+        CUDA_TRY(cudaMemcpyAsync(p->yhist + size_t(s % p->yh) * M * Fy, ys_dev + size_t(s - p->t_next) * M * Fy,
+                                 size_t(M) * Fy * 4, cudaMemcpyDeviceToDevice, p->stream));
     }
     if (outs && outs != outs_dev)
       CUDA_TRY(cudaMemcpyAsync(outs, outs_dev, size_t(n) * M * F * 4, d2h, p->stream));

@@ -112,11 +112,13 @@ class Pipeline:
                              f"does not end in {dims[0]}")
         self.M = 1 if len(si_shape) == 1 else si_shape[0]
         self._squeeze = len(si_shape) == 1
+        # targets: the output vector for mse, one class index per sample for softmax-CE
+        self.Fy = 1 if model.loss == "softmax_ce" else dims[-1]
         if sample_target is not None:
             st = tuple(np.shape(sample_target)) if not _is_cuda(sample_target) else tuple(sample_target.shape)
-            if st[-1] != dims[-1] or int(np.prod(st)) != self.M * dims[-1]:
+            if int(np.prod(st)) != self.M * self.Fy or (self.Fy > 1 and st[-1] != dims[-1]):
                 raise ValueError(f"shape inference failed at the stage-D output: sample_target {st} "
-                                 f"vs output [{self.M}, {dims[-1]}]")
+                                 f"vs targets [{self.M}, {self.Fy}]")
         self.model = model
         self.plan = plan
         self.units = units
@@ -195,8 +197,8 @@ class Pipeline:
         y = None if target_t is None else _f32(target_t)
         if x is not None and int(np.prod(tuple(x.shape))) != M * self.dims[0]:
             raise ValueError(f"x_t has shape {tuple(x.shape)}, expected [{M}, {self.dims[0]}]")
-        if y is not None and int(np.prod(tuple(y.shape))) != M * F:
-            raise ValueError(f"target_t has shape {tuple(y.shape)}, expected [{M}, {F}]")
+        if y is not None and int(np.prod(tuple(y.shape))) != M * self.Fy:
+            raise ValueError(f"target_t has shape {tuple(y.shape)}, expected [{M}, {self.Fy}]")
         if dev:
             out = torch.empty((M, F), dtype=torch.float32, device=x.device if x is not None else y.device)
             loss = torch.empty(1, dtype=torch.float32, device=out.device)
@@ -218,7 +220,8 @@ class Pipeline:
         return PipelineOutput(step=t, output=o, loss=lval, valid=v, source_sample_id=t - (self.D - 1))
 
     def run(self, xs, ys=None, n=None):
-        """n ticks with no per-tick host round trip (pt_run). xs [n, M, d0], ys [n, M, F].
+        """n ticks with no per-tick host round trip (pt_run). xs [n, M, d0], ys [n, M, F]
+        (mse) or [n, M] class indices (softmax_ce).
         numpy inputs take the host path; CUDA tensors run asynchronously on the device.
         Returns (outs [n, M, F], losses [n], valid [n])."""
         n = int(n if n is not None else (xs.shape[0] if xs is not None else ys.shape[0]))

@@ -34,18 +34,33 @@ class Pipeline:
                  sample_target=None, optim_settings=None, act_delay=1):
         import torch
 
-        if loss_fn is not None and not isinstance(loss_fn, torch.nn.MSELoss):
-            raise NotImplementedError("only torch.nn.MSELoss (mean) is implemented on the B200 path")
-        if loss_fn is not None and getattr(loss_fn, "reduction", "mean") != "mean":
-            raise NotImplementedError("MSELoss must use reduction='mean' (SPEC.md:74)")
-        lr = 1e-3
+        loss = "mse"
+        if loss_fn is not None:
+            if isinstance(loss_fn, torch.nn.CrossEntropyLoss):
+                loss = "softmax_ce"  # targets: class indices
+                if getattr(loss_fn, "label_smoothing", 0.0) or loss_fn.weight is not None \
+                        or loss_fn.ignore_index >= 0 and loss_fn.ignore_index != -100:
+                    raise NotImplementedError("CrossEntropyLoss options other than the defaults are not implemented")
+            elif not isinstance(loss_fn, torch.nn.MSELoss):
+                raise NotImplementedError("only torch.nn.MSELoss and torch.nn.CrossEntropyLoss are implemented "
+                                          "on the B200 path")
+            if getattr(loss_fn, "reduction", "mean") != "mean":
+                raise NotImplementedError("the loss must use reduction='mean' (SPEC.md:74)")
+        lr, opt = 1e-3, "sgd"
         if optim_settings is not None:
             cls, hp = optim_settings
-            if cls is not torch.optim.SGD:
+            if cls is torch.optim.SGD:
+                extra = {k: v for k, v in hp.items() if k not in ("lr",) and v not in (0, 0.0, False, None)}
+                if extra:
+                    raise NotImplementedError(f"SGD options {sorted(extra)} are not implemented on the B200 path")
+            elif cls is torch.optim.Adam:
+                opt = "adam"  # beta = (0.9, 0.999), eps = 1e-8
+                betas = tuple(hp.get("betas", (0.9, 0.999)))
+                bad = {k for k, v in hp.items() if k not in ("lr", "betas", "eps") and v not in (0, 0.0, False, None)}
+                if betas != (0.9, 0.999) or float(hp.get("eps", 1e-8)) != 1e-8 or bad:
+                    raise NotImplementedError("Adam runs with betas=(0.9, 0.999), eps=1e-8 and no other options")
+            else:
                 raise NotImplementedError(f"optimizer {cls.__name__} is not implemented on the B200 path")
-            extra = {k: v for k, v in hp.items() if k not in ("lr",) and v not in (0, 0.0, False, None)}
-            if extra:
-                raise NotImplementedError(f"SGD options {sorted(extra)} are not implemented on the B200 path")
             lr = float(hp.get("lr", lr))
         devs = [torch.device(d) for d in devices] if devices else [torch.device("cuda", torch.cuda.current_device())]
         if len({(d.type, d.index if d.index is not None else torch.cuda.current_device()) for d in devs}) != 1:
@@ -55,11 +70,12 @@ class Pipeline:
         self.device = devs[0]
         self.net = net
         model = sequential_to_model(net)
+        model.loss = loss
         plan = StagePlan.from_counts(list(balance))
         si = sample_input.detach().cpu().numpy() if hasattr(sample_input, "detach") else sample_input
         st = sample_target.detach().cpu().numpy() if hasattr(sample_target, "detach") else sample_target
         with torch.cuda.device(self.device):
-            self._eng = _Engine(model, plan, "sgd", lr, si, st, act_delay=act_delay)
+            self._eng = _Engine(model, plan, opt, lr, si, st, act_delay=act_delay)
         mods = list(net)
         self.stages, a = [], 0
         for h, c in enumerate(balance):

@@ -26,10 +26,10 @@ def spec_bounds(m, counts):
     return b
 
 
-def run_oracle(m, counts, xs, ys, lr, dtype=np.float64, act_delay=1, learn=True, loss="mse"):
+def run_oracle(m, counts, xs, ys, lr, dtype=np.float64, act_delay=1, learn=True, loss="mse", optimizer="sgd"):
     layers = oracle_layers(m, dtype)
     p = oeng.Pipeline(layers, spec_bounds(m, counts), lr, xs[0].astype(dtype), ys[0].astype(dtype),
-                      loss=loss, act_delay=act_delay, learn=learn)
+                      loss=loss, act_delay=act_delay, learn=learn, optimizer=optimizer)
     outs, losses, valid = [], [], []
     for t in range(len(xs)):
         o = p.step(xs[t].astype(dtype), ys[t].astype(dtype))

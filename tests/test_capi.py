@@ -56,11 +56,17 @@ def test_create_validation(dims, sfl, kw, msg):
     assert rc == _lib.PT_EINVAL and msg in lib.pt_last_error().decode()
 
 
-def test_unsupported_reference_features():
+def test_adam_and_softmax_ce_pass_validation():
+    """Adam and softmax cross-entropy are implemented: the config validates (without a GPU
+    pt_create then fails with PT_ECUDA, never PT_EINVAL / PT_EUNSUPPORTED)."""
     lib = _lib.load()
-    cfg, keep = _cfg([4, 4], [0, 1], loss=1)
-    h = ctypes.c_void_p()
-    assert lib.pt_create(ctypes.byref(cfg), ctypes.byref(h)) == _lib.PT_EUNSUPPORTED
+    for kw in (dict(loss=1), dict(optimizer=1), dict(loss=1, optimizer=1, batch=4)):
+        cfg, keep = _cfg([4, 4], [0, 1], **kw)
+        h = ctypes.c_void_p()
+        rc = lib.pt_create(ctypes.byref(cfg), ctypes.byref(h))
+        assert rc not in (_lib.PT_EINVAL, _lib.PT_EUNSUPPORTED), lib.pt_last_error()
+        if rc == _lib.PT_OK:
+            lib.pt_destroy(h)
 
 
 def test_no_cpu_fallback_without_gpu():
