@@ -62,3 +62,44 @@ def test_mlp_costs_and_c5_plan():
         counts, best = partition.balance(costs, D)
         assert sum(counts) == 24 and len(counts) == D
         assert best >= sum(costs) / D
+
+
+# ---- CostProfile / balance_profile / assign_workers
+
+def _profile(f, b=None, bb=None, tpb=0.0, hc=None):
+    L = len(f)
+    return partition.CostProfile(list(f), list(b if b is not None else [0.0] * L),
+                                 list(bb if bb is not None else [0] * L), tpb, list(hc or []))
+
+
+def test_balance_profile_modes_and_prediction():
+    prof = _profile([3, 1, 1, 3], [0, 0, 0, 0])
+    plan = partition.balance_profile(prof, 2, "inference")
+    assert plan.layer_counts() == [2, 2] and plan.predicted_stage_cost == [4, 4]
+    # learning adds the backward cost
+    prof = _profile([1, 1, 1, 1], [5, 0, 0, 0])
+    plan = partition.balance_profile(prof, 2, "learning")
+    assert plan.layer_counts() == [1, 3] and max(plan.predicted_stage_cost) == 6
+    # transfer charged downstream: bytes * seconds/byte on the stage after the boundary
+    prof = _profile([2, 2, 2, 2], bb=[0, 100, 0, 0], tpb=0.01)
+    plan = partition.balance_profile(prof, 2, "inference")
+    assert plan.predicted_stage_cost[1] == 4 + (1.0 if plan.layer_counts()[0] == 2 else 0.0)
+    with pytest.raises(ValueError):
+        partition.balance_profile(prof, 2, "training")
+
+
+def test_cost_profile_invariants():
+    with pytest.raises(ValueError):
+        _profile([1, -1])
+    with pytest.raises(ValueError):
+        partition.CostProfile([1, 1], [1], [0, 0], 0.0)
+
+
+def test_assign_workers_examples():
+    plan = partition.balance_profile(_profile([1, 1, 1, 1]), 4, "inference")
+    assert partition.assign_workers(plan, _profile([1, 1, 1, 1], hc=[2, 2, 2, 2])).worker_assignment == [0, 1, 2, 3]
+    # host_copy_cost [5, 1, 1, 5]: stage 1 and stage D on workers 2 and 3 (1-based)
+    a = partition.assign_workers(plan, _profile([1, 1, 1, 1], hc=[5, 1, 1, 5])).worker_assignment
+    assert {a[0], a[3]} == {1, 2} and sorted(a) == [0, 1, 2, 3]
+    # 4 stages on 2 workers -> round-robin [1, 2, 1, 2] (0-based [0, 1, 0, 1])
+    assert partition.assign_workers(plan, _profile([1, 1, 1, 1], hc=[1, 1]), n_workers=2).worker_assignment == [0, 1, 0, 1]
