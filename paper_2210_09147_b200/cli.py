@@ -22,8 +22,9 @@ def _widths(spec):
     return [int(v) for v in spec.split(",")]
 
 
-def cmd_balance(args, out=sys.stdout):
+def cmd_balance(args, out=None):
     """prints the layer-count list and the predicted stage costs."""
+    out = out or sys.stdout
     import numpy as np
     from . import model as mdl, partition
     m = mdl.mlp(_widths(args.widths), act=args.act, seed=args.seed, init=args.profile_iters > 0)
@@ -48,8 +49,9 @@ def cmd_balance(args, out=sys.stdout):
     return 0
 
 
-def cmd_simulate(args, out=sys.stdout):
+def cmd_simulate(args, out=None):
     """thin wrapper over schedsim."""
+    out = out or sys.stdout
     from . import schedsim
     pol = schedsim.SchedulePolicy(args.policy, args.stages, args.steps, args.microbatches)
     events, rep = schedsim.simulate(pol)

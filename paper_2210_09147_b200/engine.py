@@ -189,6 +189,26 @@ class Pipeline:
     def t(self):
         return self._t
 
+    def timeline(self, n_samples=None):
+        """TimelineEvents (schedsim.TimelineEvent) of the ticks run so far on this process's
+        stages, for the engine/simulator agreement check. Tick t of stage h
+        forwards the activation stage h-1 produced at tick t-1 (the kernel polls inslot for
+        tag t-1; stage 1 reads x_t) and backwards the gradient stage h+1 produced at tick t-1
+        (gslot tag t-1; stage D uses its own tick's loss gradient), so by induction F is
+        sample t-(h-1) and B is sample t-2D+h+1; the update follows B on every learning tick.
+        Events whose sample is negative (warm-up) or >= n_samples are omitted."""
+        from .schedsim import TimelineEvent
+        ev = []
+        for t in range(self._t):
+            for h in range(self.local_first + 1, self.local_first + self.local_count + 1):
+                kf, kb = t - (h - 1), t - 2 * self.D + h + 1
+                if kf >= 0 and (n_samples is None or kf < n_samples):
+                    ev.append(TimelineEvent(t, h, "F", kf))
+                if self.learn and kb >= 0 and (n_samples is None or kb < n_samples):
+                    ev.append(TimelineEvent(t, h, "B", kb))
+                    ev.append(TimelineEvent(t, h, "U", kb))
+        return ev
+
     def step(self, x_t, target_t=None) -> PipelineOutput:
         """pipeline_step: one synchronous tick."""
         M, F = self.M, self.F

@@ -17,11 +17,14 @@ pytestmark = pytest.mark.gpu
 
 
 def _case(widths, counts, T, lr, act="relu", seed=0, act_delay=1, learn=True, M=1, grid=0, optimizer="sgd",
-          loss="mse"):
+          loss="mse", data=None):
     m = mdl.mlp(widths, act=act, seed=seed, loss=loss)
-    st = streams.SmoothStream(widths[0], widths[-1], seed=seed + 1, batch=M)
-    xs, ys = st.block(0, T)
-    if loss == "softmax_ce":  # class index per sample: the nearest class of the smooth target
+    if data is not None:  # (xs [T, M, d], ys [T, M(, F)]) from another stream source
+        xs, ys = data
+    else:
+        st = streams.SmoothStream(widths[0], widths[-1], seed=seed + 1, batch=M)
+        xs, ys = st.block(0, T)
+    if loss == "softmax_ce" and data is None:  # class index per sample: the nearest class of the smooth target
         ys = np.argmax(ys, axis=-1).astype(np.float64)  # [T, M]
     W0 = [l.W.astype(np.float64) for l in m.dense_layers]
     pipe = engine.Pipeline(m, counts, optimizer, lr, xs[0] if M > 1 else xs[0, 0], ys[0] if M > 1 else ys[0, 0],
@@ -338,3 +341,23 @@ def test_paper_api_adam_cross_entropy():
             continue
         assert np.allclose(pipe.outputs_buffer.cpu().numpy(), o.output[0], rtol=1e-4, atol=1e-5)
         assert abs(float(pipe.loss_buffer) - o.loss) <= 1e-4 * max(1.0, o.loss)
+
+
+def test_drift2d_stream_softmax_ce():
+    """drift2d as the input stream: 4 rotating classes, CE on the class index."""
+    xs, ys = streams.Drift2dStream(4, rho=0.05, sigma=0.1, seed=3).block(0, 40)
+    _case([2, 32, 32, 4], [2, 3], 40, 0.05, loss="softmax_ce", data=(xs, ys))
+
+
+@pytest.mark.parametrize("opt", ["sgd", "adam"])
+def test_replay_window_softmax_ce(tmp_path, opt):
+    """§5.D replay batch: a DatasetFile written and read back, the
+    W=4 sliding window as the micro-batch, CE averaged over the window."""
+    rng = np.random.default_rng(7)
+    centers = rng.standard_normal((5, 12))
+    lab = rng.integers(0, 5, 24)
+    x = (centers[lab] + 0.3 * rng.standard_normal((24, 12))).astype(np.float32)
+    streams.dataset_write(tmp_path / "ds.bin", x, lab)
+    rs = streams.ReplayStream(streams.dataset_read(tmp_path / "ds.bin"), 4, passes=2)
+    xs, ys = rs.block(0, 48)
+    _case([12, 48, 32, 5], [2, 3], 48, 0.02, M=4, loss="softmax_ce", optimizer=opt, data=(xs, ys))
