@@ -112,6 +112,11 @@ int pt_sync(pt_pipeline* p);
 /* Use an external CUDA stream (cudaStream_t as void*); NULL restores the private stream. */
 int pt_set_stream(pt_pipeline* p, void* stream);
 
+/* The stream the handle enqueues on (its private non-blocking stream unless pt_set_stream
+ * chose another). Callers passing PT_DEVICE buffers written on another stream must order that
+ * stream before pt_run/pt_step (cudaStreamWaitEvent), as the Python engine does. */
+int pt_get_stream(const pt_pipeline* p, void** stream);
+
 /* Device time (ms) of the tick kernel of the last pt_run/pt_step, from CUDA events on the
  * handle's stream; valid after pt_sync. */
 int pt_last_kernel_ms(pt_pipeline* p, float* ms);

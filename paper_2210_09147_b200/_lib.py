@@ -31,7 +31,7 @@ PT_OPT = {"sgd": 0, "adam": 1}
 # every symbol include/partime_b200.h declares (checked by tests/test_capi.py)
 EXPORTS = (
     "pt_create", "pt_set_params", "pt_get_params", "pt_step", "pt_run", "pt_sync",
-    "pt_set_stream", "pt_last_kernel_ms", "pt_tick", "pt_set_trace", "pt_get_trace",
+    "pt_set_stream", "pt_get_stream", "pt_last_kernel_ms", "pt_tick", "pt_set_trace", "pt_get_trace",
     "pt_ipc_export", "pt_ipc_import", "pt_kernel_path",
     "pt_destroy", "pt_last_error", "pt_abi_version",
 )
@@ -96,6 +96,7 @@ def load():
     lib.pt_run.argtypes = [P, P, P, ctypes.c_int64, P, P, P, ctypes.c_int32]
     lib.pt_sync.argtypes = [P]
     lib.pt_set_stream.argtypes = [P, P]
+    lib.pt_get_stream.argtypes = [P, ctypes.POINTER(ctypes.c_void_p)]
     lib.pt_last_kernel_ms.argtypes = [P, f32p]
     lib.pt_tick.argtypes = [P]
     lib.pt_tick.restype = ctypes.c_int64
@@ -109,7 +110,7 @@ def load():
     lib.pt_destroy.restype = None
     lib.pt_last_error.restype = ctypes.c_char_p
     lib.pt_abi_version.restype = ctypes.c_int32
-    for name in ("pt_set_params", "pt_get_params", "pt_step", "pt_run", "pt_sync", "pt_set_stream",
+    for name in ("pt_set_params", "pt_get_params", "pt_step", "pt_run", "pt_sync", "pt_set_stream", "pt_get_stream",
                  "pt_last_kernel_ms", "pt_ipc_export", "pt_ipc_import", "pt_set_trace", "pt_get_trace"):
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib

@@ -822,6 +822,9 @@ int run_impl(pt_pipeline* p, const float* xs, const float* ys, int64_t n, float*
   P.trace = p->d_trace;
   P.trace_cap = p->trace_cap;
   P.trace_cta = p->trace_cta;
+  if (const char* e = getenv("PT_JITTER")) P.jitter = atoi(e);
+  P.jitter_mask = 3;
+  if (const char* e = getenv("PT_JITTER_MASK")) P.jitter_mask = atoi(e);
   if (p->d_trace) CUDA_TRY(cudaMemsetAsync(p->d_trace, 0, size_t(p->trace_cap) * sizeof(u64), p->stream));
 
   if (p->tile) {
@@ -856,6 +859,9 @@ int run_impl(pt_pipeline* p, const float* xs, const float* ys, int64_t n, float*
     T.trace = p->d_trace;
     T.trace_cap = p->trace_cap;
     T.trace_cta = p->trace_cta;
+    if (const char* e = getenv("PT_JITTER")) T.jitter = atoi(e);
+    T.jitter_mask = 3;
+    if (const char* e = getenv("PT_JITTER_MASK")) T.jitter_mask = atoi(e);
     if (p->d_trace) CUDA_TRY(cudaMemsetAsync(p->d_trace, 0, size_t(p->trace_cap) * sizeof(u64), p->stream));
     CUDA_TRY(cudaMemsetAsync(p->t_bars, 0, 32 * sizeof(u64), p->stream));
     void* targs[] = {&T};
@@ -1018,6 +1024,12 @@ int pt_set_stream(pt_pipeline* p, void* stream) {
   if (!p) return fail(PT_EINVAL, "null handle");
   CUDA_TRY(cudaStreamSynchronize(p->stream));
   p->stream = stream ? reinterpret_cast<cudaStream_t>(stream) : p->own_stream;
+  return PT_OK;
+}
+
+int pt_get_stream(const pt_pipeline* p, void** stream) {
+  if (!p || !stream) return fail(PT_EINVAL, "null argument");
+  *stream = reinterpret_cast<void*>(p->stream);
   return PT_OK;
 }
 

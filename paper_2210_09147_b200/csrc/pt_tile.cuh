@@ -100,11 +100,26 @@ struct TParams {
   unsigned long long timeout_ns;
   u64* trace;  // diagnostics: (code << 56) | globaltimer of SIMT thread 0 of CTA trace_cta
   int trace_cap, trace_cta;
+  int jitter, jitter_mask;  // diagnostics: random sleeps of up to `jitter` ns at every trace
+                            // point of every role on 1 in (jitter_mask + 1) calls (race detector)
 };
 
 // SIMT group A thread 0 writes [0, cap/4), group B thread 0 [cap/4, cap/2), the MMA
 // thread [cap/2, 3cap/4), the producer [3cap/4, cap)
+__device__ __forceinline__ void t_jitter(const TParams& P, int code) {
+  uint32_t x = uint32_t(globaltimer()) ^ (blockIdx.x * 0x9E3779B9u) ^ ((threadIdx.x >> 5) * 0x85EBCA6Bu) ^
+               (uint32_t(code) * 0xC2B2AE35u);
+  x ^= x >> 16;
+  x *= 0x7FEB352Du;
+  x ^= x >> 15;
+  if ((x & uint32_t(P.jitter_mask)) == 0) {
+    const uint64_t t0 = globaltimer(), d = (x >> 8) % uint32_t(P.jitter);
+    while (globaltimer() - t0 < d) __nanosleep(1000);
+  }
+}
+
 __device__ __forceinline__ void t_trace(const TParams& P, int& idx, int code) {
+  if (P.jitter > 0) t_jitter(P, code);
   if (P.trace == nullptr || blockIdx.x != P.trace_cta) return;
   const int tid = threadIdx.x, q = P.trace_cap / 4;
   int lo;

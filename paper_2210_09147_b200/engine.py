@@ -229,7 +229,11 @@ class Pipeline:
             loss = np.empty(1, np.float32)
             valid = np.empty(1, np.int32)
             where = _lib.PT_HOST
+        if dev:
+            self._order_after_torch(out.device)
         rc = self._lib.pt_step(self._h, _ptr(x), _ptr(y), _ptr(out), _ptr(loss), _ptr(valid), where)
+        if dev:
+            self._order_torch_after(out.device)
         t = self._t
         self._t += 1
         _lib.check(rc, f"pipeline_step at step {t}")
@@ -262,8 +266,12 @@ class Pipeline:
             valid = np.empty(n, np.uint8)
             where = _lib.PT_HOST
         has_last = self.local_first + self.local_count == self.D
+        if dev:
+            self._order_after_torch(outs.device)
         rc = self._lib.pt_run(self._h, _ptr(xs), _ptr(ys), n, _ptr(outs) if has_last else None,
                               _ptr(losses) if has_last else None, _ptr(valid) if has_last else None, where)
+        if dev:
+            self._order_torch_after(outs.device)
         t0 = self._t
         self._t += n
         _lib.check(rc, f"pipeline_run at steps [{t0}, {t0 + n})")
@@ -271,6 +279,21 @@ class Pipeline:
 
     def sync(self):
         _lib.check(self._lib.pt_sync(self._h), "sync")
+
+    # ---- stream ordering with torch (device buffers) ---------------------------------------
+    def _stream(self, device):
+        raw = ctypes.c_void_p()
+        _lib.check(self._lib.pt_get_stream(self._h, ctypes.byref(raw)), "get_stream")
+        return torch.cuda.ExternalStream(raw.value or 0, device=device)
+
+    def _order_after_torch(self, device):
+        """Device inputs were written on torch's current stream (e.g. an async H2D copy):
+        the handle's stream waits for it before the kernel reads them."""
+        self._stream(device).wait_stream(torch.cuda.current_stream(device))
+
+    def _order_torch_after(self, device):
+        """Outputs are written on the handle's stream: torch's current stream waits for them."""
+        torch.cuda.current_stream(device).wait_stream(self._stream(device))
 
     def set_stream(self, stream):
         """Run on an external CUDA stream (torch.cuda.Stream or raw handle)."""
