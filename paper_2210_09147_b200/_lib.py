@@ -10,7 +10,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpartime_b200.so")
+# PT_LIBNAME selects a build variant (libpartime_b200_jitter.so: the PT_JITTER race detector)
+LIB_PATH = os.path.join(_HERE, os.environ.get("PT_LIBNAME", "libpartime_b200.so"))
 
 PT_OK = 0
 PT_EINVAL = -1

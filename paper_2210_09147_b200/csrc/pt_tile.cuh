@@ -119,7 +119,9 @@ __device__ __forceinline__ void t_jitter(const TParams& P, int code) {
 }
 
 __device__ __forceinline__ void t_trace(const TParams& P, int& idx, int code) {
+#ifdef PT_JITTER_BUILD
   if (P.jitter > 0) t_jitter(P, code);
+#endif
   if (P.trace == nullptr || blockIdx.x != P.trace_cta) return;
   const int tid = threadIdx.x, q = P.trace_cap / 4;
   int lo;

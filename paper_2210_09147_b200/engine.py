@@ -146,6 +146,7 @@ class Pipeline:
         self._h = h
         self._lib = lib
         self._t = 0
+        self._user_stream = False
         lo, hi = sfl[self.local_first], sfl[self.local_first + self.local_count]
         for j in range(lo, hi):
             self.set_layer(j, dense[j].W, dense[j].b)
@@ -229,10 +230,11 @@ class Pipeline:
             loss = np.empty(1, np.float32)
             valid = np.empty(1, np.int32)
             where = _lib.PT_HOST
-        if dev:
+        order = dev and not self._user_stream
+        if order:
             self._order_after_torch(out.device)
         rc = self._lib.pt_step(self._h, _ptr(x), _ptr(y), _ptr(out), _ptr(loss), _ptr(valid), where)
-        if dev:
+        if order:
             self._order_torch_after(out.device)
         t = self._t
         self._t += 1
@@ -266,11 +268,12 @@ class Pipeline:
             valid = np.empty(n, np.uint8)
             where = _lib.PT_HOST
         has_last = self.local_first + self.local_count == self.D
-        if dev:
+        order = dev and not self._user_stream
+        if order:
             self._order_after_torch(outs.device)
         rc = self._lib.pt_run(self._h, _ptr(xs), _ptr(ys), n, _ptr(outs) if has_last else None,
                               _ptr(losses) if has_last else None, _ptr(valid) if has_last else None, where)
-        if dev:
+        if order:
             self._order_torch_after(outs.device)
         t0 = self._t
         self._t += n
@@ -296,9 +299,13 @@ class Pipeline:
         torch.cuda.current_stream(device).wait_stream(self._stream(device))
 
     def set_stream(self, stream):
-        """Run on an external CUDA stream (torch.cuda.Stream or raw handle)."""
+        """Run on an external CUDA stream (torch.cuda.Stream or raw handle). The caller then
+        owns the ordering of device buffers against its other streams (e.g. two co-resident
+        stage handles on two streams must stay concurrent); with the private stream (None)
+        the engine orders itself after torch's current stream and torch's after the run."""
         raw = getattr(stream, "cuda_stream", stream)
         _lib.check(self._lib.pt_set_stream(self._h, ctypes.c_void_p(raw) if raw else None), "set_stream")
+        self._user_stream = bool(raw)
 
     @property
     def kernel_path(self):

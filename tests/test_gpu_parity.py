@@ -363,39 +363,6 @@ def test_replay_window_softmax_ce(tmp_path, opt):
     _case([12, 48, 32, 5], [2, 3], 48, 0.02, M=4, loss="softmax_ce", optimizer=opt, data=(xs, ys))
 
 
-@pytest.mark.parametrize("kind,counts,learn", [("tile", [7], False), ("tile", [7], True), ("tile", [4, 3], True),
-                                               ("tick", [4, 3], True), ("tick_mb", [4, 3], True)])
-def test_jitter_bitwise(kind, counts, learn, monkeypatch):
-    """Race detector: random stalls at every step phase of every warp and role (producer,
-    MMA issuer, SIMT groups / consumer warps; PT_JITTER, PT_JITTER_MASK) leave the results
-    bitwise equal to an unperturbed run, for the tcgen05 tile kernel and the tick kernel
-    (batch 1 and micro-batch). Short stalls often, long stalls (up to 0.3 ms) rarely."""
-    widths, M = {"tile": ([256, 512, 512, 256, 256], 16), "tick": ([32, 64, 64, 64, 16], 1),
-                 "tick_mb": ([64, 96, 96, 96, 32], 4)}[kind]
-    T = 16
-    st = streams.SmoothStream(widths[0], widths[-1], seed=5, batch=M)
-    xs, ys = st.block(0, T)
-    xs, ys = xs.astype(np.float32), ys.astype(np.float32)
-
-    s0 = (lambda a: a[0]) if M > 1 else (lambda a: a[0, 0])
-
-    def run():
-        p = engine.Pipeline(mdl.mlp(widths, seed=4), counts, "sgd", 0.05, s0(xs), s0(ys), learn=learn)
-        assert p.kernel_path == ("tile" if kind == "tile" else "tick")
-        o, l, _ = p.run(xs, ys)
-        W = [p.get_layer(j)[0] for j in range(p.L)]
-        p.close()
-        return o, l, W
-
-    o0, l0, W0 = run()
-    for jit, mask in (("8000", "3"), ("300000", "511")):
-        monkeypatch.setenv("PT_JITTER", jit)
-        monkeypatch.setenv("PT_JITTER_MASK", mask)
-        o, l, W = run()
-        assert np.array_equal(o, o0) and np.array_equal(l, l0, equal_nan=True)
-        assert all(np.array_equal(a, b) for a, b in zip(W, W0))
-
-
 @pytest.mark.parametrize("M", [1, 16])
 def test_device_inputs_ordered_after_torch_stream(M):
     """CUDA-tensor inputs copied asynchronously (pinned host memory, non_blocking) on a torch
