@@ -365,6 +365,19 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX, group=gloo)
         e2e_s = float(t[0])
     e2e_value = e2e_steps * T * BATCH / e2e_s
+    # the per-sample drop-in path (SURVEY.md §8(d) "two API paths"): Pipeline.step -> pt_step,
+    # host buffers, one synchronous tick per call (H2D x and y, tick, D2H output and loss)
+    step_api = None
+    if world == 1:
+        for t in range(8):
+            pipe.step(xs_h[t % T, 0], ys_h[t % T, 0])
+        n_calls = 64
+        t0 = time.perf_counter()
+        for t in range(n_calls):
+            pipe.step(xs_h[t % T, 0], ys_h[t % T, 0])
+        el = time.perf_counter() - t0
+        step_api = {"value": round(n_calls / el, 2), "unit": "samples/s", "us_per_call": round(el / n_calls * 1e6, 2),
+                    "api": "engine.Pipeline.step -> pt_step (host buffers, one synchronous tick per call)"}
     h2d = T * BATCH * (widths[0] + widths[-1]) * 4
     d2h = T * BATCH * widths[-1] * 4 + T * 4 + T
 
@@ -410,6 +423,7 @@ def main():
         # job-wide bytes: xs enter at stage 1's GPU, targets and results at stage D's
         "e2e": {"value": round(e2e_value, 2), "unit": "samples/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
+        "step_api": step_api,
         "gpu_launches": 2 * args.steps,
         "clocks": clocks,
         "other_configs": extra,
