@@ -170,6 +170,12 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* tm, const void* 
                "r"(c1), "r"(smem_u32(src))
                : "memory");
 }
+// A tensor map in global memory written by the host (cudaMemcpy) must be acquired by the
+// async proxy before TMA uses it: a new handle can reuse the address of a freed handle's map,
+// and a stale descriptor-cache entry would point the copies at the old weights.
+__device__ __forceinline__ void tma_fence_desc_acquire(const CUtensorMap* tm) {
+  asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(tm) : "memory");
+}
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* tm) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(tm) : "memory");
 }

@@ -242,6 +242,11 @@ struct TSmem {
 __device__ void t_producer(const TParams& P, const TSmem& sm) {
   const int c = blockIdx.x, G = P.G;
   uint32_t j = 0;
+  for (int s = 0; s < P.n_stages; ++s)
+    for (int i = P.stages[s].first; i < P.stages[s].first + P.stages[s].k; ++i) {
+      tma_fence_desc_acquire(P.layers[i].tmf);
+      tma_fence_desc_acquire(P.layers[i].tmb);
+    }
   // per slot: kind of the chunk it holds (1 forward: released by the MMA commit on sfree,
   // 2 backward: released by the 4 write-back warps on bfree), completions consumed, and a
   // pending write-back (layer, row, col) of an updated backward tile
