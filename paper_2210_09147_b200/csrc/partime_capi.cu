@@ -170,6 +170,10 @@ struct pt_pipeline {
   float* yhist = nullptr;
   int yh = 1;
   cudaStream_t own_stream = nullptr, stream = nullptr;
+  // pinned staging of small host-buffer calls (pt_step): pageable copies block the host for
+  // each transfer; one memcpy into pinned memory and truly asynchronous copies do not
+  float* pin = nullptr;
+  size_t pin_floats = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   bool timed = false;
   long long t_next = 0;
@@ -728,6 +732,38 @@ int run_impl(pt_pipeline* p, const float* xs, const float* ys, int64_t n, float*
   if (last && p->learn && !ys) return fail(PT_EINVAL, "targets are required for online learning (stage D)");
   const int n0 = p->dims[0], ld0 = p->stage_ld0(0);
 
+  // small host-buffer calls (pt_step and short pt_run) go through a pinned staging area:
+  // [xs n*M*n0 | ys n*M*Fy | outs n*M*F | losses n | valid n (bytes, as floats)]
+  const size_t st_x = first ? size_t(n) * M * n0 : 0, st_y = (last && ys) ? size_t(n) * M * Fy : 0;
+  const size_t st_o = (last && outs) ? size_t(n) * M * F : 0, st_l = (last && losses) ? size_t(n) : 0;
+  const size_t st_v = (last && valid) ? (size_t(n) + 3) / 4 : 0;
+  const size_t st_total = st_x + st_y + st_o + st_l + st_v;
+  const bool staged = where == PT_HOST && st_total <= (size_t(1) << 16);
+  float* pin_x = nullptr;
+  float* pin_y = nullptr;
+  float* pin_o = nullptr;
+  float* pin_l = nullptr;
+  uint8_t* pin_v = nullptr;
+  if (staged) {
+    if (p->pin_floats < st_total) {
+      CUDA_TRY(cudaStreamSynchronize(p->stream));
+      if (p->pin) CUDA_TRY(cudaFreeHost(p->pin));
+      p->pin = nullptr;
+      p->pin_floats = 0;
+      CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&p->pin), std::max<size_t>(st_total, 4096) * 4,
+                             cudaHostAllocDefault));
+      p->pin_floats = std::max<size_t>(st_total, 4096);
+    }
+    pin_x = p->pin;
+    pin_y = pin_x + st_x;
+    pin_o = pin_y + st_y;
+    pin_l = pin_o + st_o;
+    pin_v = reinterpret_cast<uint8_t*>(pin_l + st_l);
+    if (st_x) memcpy(pin_x, xs, st_x * 4);
+    if (st_y) memcpy(pin_y, ys, st_y * 4);
+    if (st_x) xs = pin_x;
+    if (st_y) ys = pin_y;
+  }
   if (first) {
     PT_TRY(ensure(p, &p->xs_pad, &p->xs_cap, size_t(n), size_t(M) * ld0));
     CUDA_TRY(cudaMemcpy2DAsync(p->xs_pad, size_t(ld0) * 4, xs, size_t(n0) * 4, size_t(n0) * 4, size_t(n) * M,
@@ -894,15 +930,20 @@ int run_impl(pt_pipeline* p, const float* xs, const float* ys, int64_t n, float*
                                  size_t(M) * Fy * 4, cudaMemcpyDeviceToDevice, p->stream));
     }
     if (outs && outs != outs_dev)
-      CUDA_TRY(cudaMemcpyAsync(outs, outs_dev, size_t(n) * M * F * 4, d2h, p->stream));
+      CUDA_TRY(cudaMemcpyAsync(staged ? pin_o : outs, outs_dev, size_t(n) * M * F * 4, d2h, p->stream));
     if (losses && losses != losses_dev)
-      CUDA_TRY(cudaMemcpyAsync(losses, losses_dev, size_t(n) * 4, d2h, p->stream));
+      CUDA_TRY(cudaMemcpyAsync(staged ? pin_l : losses, losses_dev, size_t(n) * 4, d2h, p->stream));
     if (valid && valid != valid_dev)
-      CUDA_TRY(cudaMemcpyAsync(valid, valid_dev, size_t(n), d2h, p->stream));
+      CUDA_TRY(cudaMemcpyAsync(staged ? pin_v : valid, valid_dev, size_t(n), d2h, p->stream));
   }
   p->t_next += n;
   if (where == PT_HOST) {
     CUDA_TRY(cudaStreamSynchronize(p->stream));
+    if (staged && last) {
+      if (st_o) memcpy(outs, pin_o, st_o * 4);
+      if (st_l) memcpy(losses, pin_l, st_l * 4);
+      if (st_v) memcpy(valid, pin_v, size_t(n));
+    }
     return read_status(p);
   }
   return PT_OK;
@@ -940,6 +981,7 @@ void pt_destroy(pt_pipeline* p) {
   if (p->ev0) cudaEventDestroy(p->ev0);
   if (p->ev1) cudaEventDestroy(p->ev1);
   if (p->own_stream) cudaStreamDestroy(p->own_stream);
+  if (p->pin) cudaFreeHost(p->pin);
   delete p;
 }
 
