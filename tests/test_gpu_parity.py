@@ -389,3 +389,39 @@ def test_device_inputs_ordered_after_torch_stream(M):
     side.synchronize()
     assert np.array_equal(o_host.numpy(), o_ref) and np.array_equal(l.cpu().numpy(), l_ref, equal_nan=True)
     p.close()
+
+
+def test_run_with_D_minus_1_steps_has_no_valid_output():
+    """n_steps = D-1 yields 0 valid outputs; RunReport CSV rows match."""
+    m = mdl.mlp([16, 32, 32, 8], seed=1)
+    st = streams.SmoothStream(16, 8, seed=2)
+    xs, ys = st.block(0, 1)
+    p = engine.Pipeline(m, [2, 2, 1], "sgd", 0.01, xs[0, 0], ys[0, 0])
+    rep = engine.pipeline_run(p, streams.SmoothStream(16, 8, seed=2), 2)
+    assert rep.valid_outputs == 0 and len(rep.steps) == 2
+    rows = list(rep.csv_rows())
+    assert rows[0] == "step,sample_id,loss,valid,step_wall_seconds" and len(rows) == 3
+    rep = engine.pipeline_run(p, streams.SmoothStream(16, 8, seed=2), 3)
+    assert rep.valid_outputs == 3  # steps 2, 3, 4 of the same pipeline are past the warm-up
+    p.close()
+
+
+@pytest.mark.parametrize("D", [2, 3, 4])
+def test_frozen_weights_output_equals_sequential(D):
+    """Acceptance criterion 1 on the device: with lr = 0 the D-stage output at
+    tick t is the D=1 output of sample t-(D-1), bit for bit (same kernel, same row split)."""
+    widths = [64, 128, 128, 128, 96, 32]
+    m = mdl.mlp(widths, seed=3)
+    st = streams.SmoothStream(widths[0], widths[-1], seed=4)
+    T = 12
+    xs, ys = st.block(0, T)
+    xs, ys = xs.astype(np.float32), ys.astype(np.float32)
+    ref = engine.Pipeline(m, [len(m.layers)], "sgd", 0.0, xs[0, 0], ys[0, 0])
+    o1, _, _ = ref.run(xs, ys)
+    ref.close()
+    counts = {2: [4, 5], 3: [4, 2, 3], 4: [2, 2, 2, 3]}[D]
+    p = engine.Pipeline(m, counts, "sgd", 0.0, xs[0, 0], ys[0, 0])
+    oD, _, valid = p.run(xs, ys)
+    p.close()
+    assert not valid[:D - 1].any() and valid[D - 1:].all()
+    assert np.array_equal(oD[D - 1:], o1[:T - (D - 1)])
