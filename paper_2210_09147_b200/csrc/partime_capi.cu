@@ -128,6 +128,7 @@ struct StageHost {
   char* down = nullptr;  // downstream stage's comm block, h < D
   int G_up = 0, G_down = 0;
   bool up_remote = false, down_remote = false;
+  int cta0 = 0, ncta = 0;  // the CTAs that run this stage (all, unless stages run concurrently)
   // micro-batch tile path (plain fp32 buffers): cache[2] slots of a_0..a_k, inslot[2], gslot[2]
   float* tcache = nullptr;
   size_t tcache_floats = 0;
@@ -153,6 +154,15 @@ struct pt_pipeline {
   pt::LayerDev* d_layers = nullptr;
   pt::StageDev* d_stages = nullptr;
   u64* d_tick_end = nullptr;
+  // local stages on disjoint SM partitions (PT_CONC=0: every CTA runs every stage in turn)
+  bool conc = false;
+  std::vector<int> stage_cta0, stage_ncta;  // per local stage
+  int layer_ncta(size_t li) const {         // CTAs sharing local layer li's rows
+    for (int s = 0; s < local_count; ++s)
+      if (int(li) + layer_base >= sfl[local_first + s] && int(li) + layer_base < sfl[local_first + s + 1])
+        return stage_ncta[s];
+    return G;
+  }
   int* d_status = nullptr;
   long long* d_first_bad = nullptr;
   float* xs_pad = nullptr;
@@ -286,6 +296,8 @@ int upload_desc(pt_pipeline* p) {
     d.k = h.k;
     d.G_up = h.G_up;
     d.G_down = h.G_down;
+    d.cta0 = h.cta0;
+    d.ncta = h.ncta;
     d.up_remote = h.up_remote ? 1 : 0;
     d.down_remote = h.down_remote ? 1 : 0;
     d.ld0 = h.ld0;
@@ -351,9 +363,11 @@ int validate(const pt_config* c, std::string* why) {
 // Shared-memory plan: the ring gets every byte the small buffers do not need.
 int plan_smem(pt_pipeline* p) {
   int max_ld = 128, maxrows = 1, sp_max = 1;
-  for (const LayerHost& Lh : p->layers) {
+  for (size_t li = 0; li < p->layers.size(); ++li) {
+    const LayerHost& Lh = p->layers[li];
+    const int g = p->layer_ncta(li);
     max_ld = std::max(max_ld, Lh.ld_in);
-    maxrows = std::max(maxrows, (Lh.n_out + p->G - 1) / p->G);
+    maxrows = std::max(maxrows, (Lh.n_out + g - 1) / g);
   }
   // Ring geometry: 4 x 32 KB slots, measured best for the 2048-wide learning tick
   // (profiles/round1_ring_sweep.md). 3 x 64 KB with one copy in flight per SM streams
@@ -382,7 +396,8 @@ int plan_smem(pt_pipeline* p) {
   auto a128 = [](size_t v) { return int(align_up(v, 128)); };
   int off = 0;  // ring size decided last; lay out the tail from a fixed budget
   size_t bias_rows = 0;
-  for (const LayerHost& Lh : p->layers) bias_rows += (Lh.n_out + p->G - 1) / p->G;
+  for (size_t li = 0; li < p->layers.size(); ++li)
+    bias_rows += (p->layers[li].n_out + p->layer_ncta(li) - 1) / p->layer_ncta(li);
   const int n_stages_local = p->local_count;
   const int desc_bytes = a128(p->layers.size() * sizeof(pt::LayerDev) + n_stages_local * sizeof(pt::StageDev) +
                               p->layers.size() * sizeof(int));
@@ -606,6 +621,55 @@ int create_impl(const pt_config* c, pt_pipeline* p) {
     }
     p->layers.push_back(Lh);
   }
+  // Local stages are independent within a tick (each reads only tick t-1 data), so with
+  // several of them on this GPU they run concurrently on disjoint CTA ranges, sized by their
+  // weight bytes, and exchange through L2 exactly as separate GPUs would through NVLink
+  p->stage_cta0.assign(p->local_count, 0);
+  p->stage_ncta.assign(p->local_count, p->G);
+  p->conc = p->local_count > 1 && !p->tile && p->G >= 2 * p->local_count;
+  // uniform widths only: with uneven layers (C5) a byte-proportional split leaves the stage
+  // with the most lock-step steps per byte behind, measured slower than running in turn
+  for (const LayerHost& Lh : p->layers)
+    p->conc = p->conc && Lh.n_in == p->layers[0].n_in && Lh.n_out == p->layers[0].n_out;
+  if (const char* e = getenv("PT_CONC")) p->conc = p->conc && atoi(e) != 0;
+  if (p->conc) {
+    std::vector<double> w(p->local_count, 0.0);
+    double tot = 0.0;
+    for (int s = 0; s < p->local_count; ++s) {
+      for (int l = p->sfl[p->local_first + s]; l < p->sfl[p->local_first + s + 1]; ++l)
+        w[s] += double(p->dims[l]) * double(p->dims[l + 1]);
+      tot += w[s];
+    }
+    std::vector<double> frac(p->local_count);
+    int used = 0;
+    for (int s = 0; s < p->local_count; ++s) {
+      const double x = p->G * w[s] / tot;
+      p->stage_ncta[s] = std::max(1, int(x));
+      frac[s] = x - int(x);
+      used += p->stage_ncta[s];
+    }
+    while (used < p->G) {  // largest remainders first
+      int best = 0;
+      for (int s = 1; s < p->local_count; ++s)
+        if (frac[s] > frac[best]) best = s;
+      ++p->stage_ncta[best];
+      frac[best] = -1.0;
+      ++used;
+    }
+    while (used > p->G) {  // (minimum-1 rounding overshoot) take from the largest
+      int big = 0;
+      for (int s = 1; s < p->local_count; ++s)
+        if (p->stage_ncta[s] > p->stage_ncta[big]) big = s;
+      --p->stage_ncta[big];
+      --used;
+    }
+    for (int s = 1; s < p->local_count; ++s) p->stage_cta0[s] = p->stage_cta0[s - 1] + p->stage_ncta[s - 1];
+    if (plan_smem(p) != PT_OK) {  // rows per CTA too many for shared memory: run in turn
+      p->conc = false;
+      p->stage_cta0.assign(p->local_count, 0);
+      p->stage_ncta.assign(p->local_count, p->G);
+    }
+  }
   PT_TRY(plan_smem(p));
   for (LayerHost& Lh : p->layers) Lh.rows_per_chunk = p->slot_floats / Lh.ld_in;
   // local stages
@@ -617,6 +681,8 @@ int create_impl(const pt_config* c, pt_pipeline* p) {
     S.first_local = S.first_global - p->layer_base;
     S.ld0 = p->stage_ld0(s0);
     S.ldk = p->stage_ldk(s0);
+    S.cta0 = p->stage_cta0[s0 - s_lo];
+    S.ncta = p->stage_ncta[s0 - s_lo];
     // cache slot: a_0 .. a_k, each [M][ld]
     size_t off = 0;
     for (int i = 0; i < S.k; ++i) {
@@ -646,11 +712,11 @@ int create_impl(const pt_config* c, pt_pipeline* p) {
     StageHost& S = p->stages[s];
     if (s > 0) {
       S.up = p->stages[s - 1].comm;
-      S.G_up = p->G;
+      S.G_up = p->stages[s - 1].ncta;
     }
     if (s + 1 < p->stages.size()) {
       S.down = p->stages[s + 1].comm;
-      S.G_down = p->G;
+      S.G_down = p->stages[s + 1].ncta;
     }
   }
   PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&p->d_layers), p->layers.size() * sizeof(pt::LayerDev)));
@@ -1125,7 +1191,7 @@ int pt_ipc_export(pt_pipeline* p, int32_t stage, void* buf, size_t cap, size_t* 
   b.magic = PT_IPC_MAGIC;
   b.abi = PT_ABI_VERSION;
   b.stage = stage;
-  b.G = p->G;
+  b.G = S.ncta > 0 ? S.ncta : p->G;
   b.M = p->M;
   b.ld0 = S.ld0;
   b.ldk = S.ldk;

@@ -53,11 +53,41 @@ def test_ipc_stage_handles_match_single_handle(widths, counts, T, M, grid):
     a.sync()
     b.sync()
     ref = engine.Pipeline(mdl.mlp(widths, seed=4), counts, "sgd", 0.05, _sample(xs, M), _sample(ys, M),
-                          grid=grid)  # same work split
+                          grid=grid)  # same work split (stages in turn on all `grid` CTAs)
     o, l, _ = ref.run(xs, ys)
     assert np.array_equal(outs.cpu().numpy(), o) and np.array_equal(losses.cpu().numpy(), l, equal_nan=True)
     W = [ref.get_layer(j) for j in range(ref.L)]
     mine = [a.get_layer(j) for j in a._local_units()] + [b.get_layer(j) for j in b._local_units()]
     assert all(np.array_equal(x, y) for (x, _), (y, _) in zip(mine, W))
     for p in (a, b, ref):
+        p.close()
+
+
+def test_concurrent_stages_match_two_handles():
+    """One handle with two local stages of equal bytes runs them concurrently, 74 CTAs each
+    (DESIGN.md §4.1). Its result must equal two co-resident single-stage handles of 74 CTAs
+    exchanging through the IPC path, bit for bit: the same row split, the same protocol."""
+    import torch
+    from paper_2210_09147_b200 import engine, model as mdl, streams
+    widths, counts, T = [256] * 7, [6, 5], 16  # 3 + 3 dense layers of 256 x 256
+    st = streams.SmoothStream(widths[0], widths[-1], seed=5)
+    xs, ys = st.block(0, T)
+    xs, ys = xs.astype(np.float32), ys.astype(np.float32)
+    m, a, b = _stage_pair(widths, counts, 0.05, xs, ys, grid=74)
+    sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
+    a.set_stream(sa)
+    b.set_stream(sb)
+    xd, yd = torch.from_numpy(xs).cuda(), torch.from_numpy(ys).cuda()
+    torch.cuda.synchronize()
+    a.run(xd, None, T)
+    outs, losses, _ = b.run(None, yd, T)
+    a.sync()
+    b.sync()
+    one = engine.Pipeline(mdl.mlp(widths, seed=4), counts, "sgd", 0.05, xs[0, 0], ys[0, 0], grid=148)
+    o, l, _ = one.run(xs, ys)
+    assert np.array_equal(outs.cpu().numpy(), o) and np.array_equal(losses.cpu().numpy(), l, equal_nan=True)
+    W = [one.get_layer(j) for j in range(one.L)]
+    mine = [a.get_layer(j) for j in a._local_units()] + [b.get_layer(j) for j in b._local_units()]
+    assert all(np.array_equal(x, y) for (x, _), (y, _) in zip(mine, W))
+    for p in (a, b, one):
         p.close()

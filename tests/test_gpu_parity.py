@@ -425,3 +425,9 @@ def test_frozen_weights_output_equals_sequential(D):
     p.close()
     assert not valid[:D - 1].any() and valid[D - 1:].all()
     assert np.array_equal(oD[D - 1:], o1[:T - (D - 1)])
+
+
+@pytest.mark.parametrize("D,counts", [(2, [8, 7]), (3, [6, 4, 5]), (4, [4, 4, 4, 3])])
+def test_concurrent_stages(D, counts):
+    """Uniform widths: the local stages run concurrently on disjoint CTA ranges."""
+    _case([128] * 9, counts, 40, 0.02)
