@@ -577,12 +577,16 @@ int create_impl(const pt_config* c, pt_pipeline* p) {
   CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device));
   CUDA_TRY(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, p->device));
   if (!coop) return fail(PT_EUNSUPPORTED, "device does not support cooperative launch");
-  CUDA_TRY(cudaFuncSetAttribute(pt::tick_kernel<true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, pt::SMEM_MAX));
-  CUDA_TRY(cudaFuncSetAttribute(pt::tick_kernel<true, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, pt::SMEM_MAX));
-  CUDA_TRY(cudaFuncSetAttribute(pt::tick_kernel<false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, pt::SMEM_MAX));
-  CUDA_TRY(cudaFuncSetAttribute(pt::tick_kernel<false, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, pt::SMEM_MAX));
+  {
+    const void* fns[] = {(const void*)pt::tick_kernel<true, 4, false>, (const void*)pt::tick_kernel<true, 8, false>,
+                         (const void*)pt::tick_kernel<false, 4, false>, (const void*)pt::tick_kernel<false, 8, false>,
+                         (const void*)pt::tick_kernel<true, 4, true>, (const void*)pt::tick_kernel<true, 8, true>,
+                         (const void*)pt::tick_kernel<false, 4, true>, (const void*)pt::tick_kernel<false, 8, true>};
+    for (const void* f : fns)
+      CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, pt::SMEM_MAX));
+  }
   int per_sm = 0;
-  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pt::tick_kernel<true, 8>, pt::NTHREADS,
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pt::tick_kernel<true, 8, false>, pt::NTHREADS,
                                                          pt::SMEM_MAX));
   if (per_sm < 1) return fail(PT_EUNSUPPORTED, "tick kernel does not fit on one SM");
   p->G = c->grid > 0 ? c->grid : sms;
@@ -974,8 +978,13 @@ int run_impl(pt_pipeline* p, const float* xs, const float* ys, int64_t n, float*
   } else {
     void* args[] = {&P};
     CUDA_TRY(cudaEventRecord(p->ev0, p->stream));
-    const void* fn = p->fast ? (p->qw == 8 ? (const void*)pt::tick_kernel<true, 8> : (const void*)pt::tick_kernel<true, 4>)
-                             : (p->qw == 8 ? (const void*)pt::tick_kernel<false, 8> : (const void*)pt::tick_kernel<false, 4>);
+    const void* fn;
+    if (p->conc)
+      fn = p->fast ? (p->qw == 8 ? (const void*)pt::tick_kernel<true, 8, true> : (const void*)pt::tick_kernel<true, 4, true>)
+                   : (p->qw == 8 ? (const void*)pt::tick_kernel<false, 8, true> : (const void*)pt::tick_kernel<false, 4, true>);
+    else
+      fn = p->fast ? (p->qw == 8 ? (const void*)pt::tick_kernel<true, 8, false> : (const void*)pt::tick_kernel<true, 4, false>)
+                   : (p->qw == 8 ? (const void*)pt::tick_kernel<false, 8, false> : (const void*)pt::tick_kernel<false, 4, false>);
     CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(p->G), dim3(pt::NTHREADS), args, size_t(p->smem_bytes), p->stream));
     CUDA_TRY(cudaEventRecord(p->ev1, p->stream));
   }
