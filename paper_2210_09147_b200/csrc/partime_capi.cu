@@ -156,6 +156,12 @@ struct pt_pipeline {
   u64* d_tick_end = nullptr;
   // local stages on disjoint SM partitions (PT_CONC=0: every CTA runs every stage in turn)
   bool conc = false;
+  // Work issued on the legacy default stream (cudaMemset of new buffers, cudaMemcpy of
+  // parameters and descriptors) is not ordered before the handle's non-blocking stream, and
+  // a pageable H2D cudaMemcpy may return before its DMA lands: the next launch waits for it.
+  // Without that, a kernel could read recycled memory that still holds another pipeline's
+  // tagged words (a stale tag can match a tick) or weights that are not there yet.
+  bool legacy_dirty = true;
   std::vector<int> stage_cta0, stage_ncta;  // per local stage
   int layer_ncta(size_t li) const {         // CTAs sharing local layer li's rows
     for (int s = 0; s < local_count; ++s)
@@ -239,6 +245,7 @@ int dev_alloc(pt_pipeline* p, void** ptr, size_t bytes) {
   if (bytes == 0) bytes = 16;
   CUDA_TRY(cudaMalloc(ptr, bytes));
   CUDA_TRY(cudaMemset(*ptr, 0, bytes));
+  p->legacy_dirty = true;
   p->allocs.push_back(*ptr);
   return PT_OK;
 }
@@ -259,6 +266,9 @@ int ensure(pt_pipeline* p, T** buf, size_t* cap, size_t need, size_t elems_per) 
   *buf = nullptr;
   size_t n = std::max<size_t>(need, 64);
   PT_TRY(dev_alloc(p, reinterpret_cast<void**>(buf), n * elems_per * sizeof(T)));
+  // the buffer is filled on the handle's stream right away: its zeroing (legacy stream) must
+  // not land after that
+  CUDA_TRY(cudaStreamSynchronize(0));
   *cap = n;
   return PT_OK;
 }
@@ -323,6 +333,7 @@ int upload_desc(pt_pipeline* p) {
   }
   CUDA_TRY(cudaMemcpy(p->d_layers, ld.data(), ld.size() * sizeof(pt::LayerDev), cudaMemcpyHostToDevice));
   CUDA_TRY(cudaMemcpy(p->d_stages, sd.data(), sd.size() * sizeof(pt::StageDev), cudaMemcpyHostToDevice));
+  p->legacy_dirty = true;
   return PT_OK;
 }
 
@@ -485,6 +496,7 @@ int upload_tile_stages(pt_pipeline* p) {
     (void)M;
   }
   CUDA_TRY(cudaMemcpy(p->d_tstages, ts.data(), ts.size() * sizeof(pt::TStage), cudaMemcpyHostToDevice));
+  p->legacy_dirty = true;
   return PT_OK;
 }
 
@@ -538,6 +550,7 @@ int setup_tile(pt_pipeline* p) {
   PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&p->d_tstages), p->stages.size() * sizeof(pt::TStage)));
   CUDA_TRY(cudaMemcpy(p->d_tmaps, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
   CUDA_TRY(cudaMemcpy(p->d_tlayers, tl.data(), tl.size() * sizeof(pt::TLayer), cudaMemcpyHostToDevice));
+  p->legacy_dirty = true;
   p->t_layers_host = tl;
   PT_TRY(upload_tile_stages(p));
   // shared memory: 1 KB alignment slack, ring, lo, operands, delta tile, reductions, barriers
@@ -783,6 +796,7 @@ int read_status(pt_pipeline* p) {
   if (bad != std::numeric_limits<long long>::max()) {
     const long long big = std::numeric_limits<long long>::max();
     CUDA_TRY(cudaMemcpy(p->d_first_bad, &big, sizeof(big), cudaMemcpyHostToDevice));
+    p->legacy_dirty = true;
     return fail(PT_ENONFINITE, "non-finite loss at step " + std::to_string(bad));
   }
   return PT_OK;
@@ -792,6 +806,10 @@ int run_impl(pt_pipeline* p, const float* xs, const float* ys, int64_t n, float*
              uint8_t* valid, int where) {
   PT_TRY(check_ready(p));
   if (n <= 0) return PT_OK;
+  if (p->legacy_dirty) {
+    CUDA_TRY(cudaStreamSynchronize(0));
+    p->legacy_dirty = false;
+  }
   if (n > (1 << 30)) return fail(PT_EINVAL, "too many ticks in one call");
   if (where != PT_HOST && where != PT_DEVICE) return fail(PT_EINVAL, "where must be PT_HOST or PT_DEVICE");
   const cudaMemcpyKind h2d = where == PT_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
@@ -1073,6 +1091,7 @@ int pt_set_params(pt_pipeline* p, int32_t layer, const float* W, const float* b,
     CUDA_TRY(cudaMemcpy2D(Lh->W, size_t(Lh->ld_in) * 4, W, size_t(Lh->n_in) * 4, size_t(Lh->n_in) * 4,
                           size_t(Lh->n_out), k));
   if (b) CUDA_TRY(cudaMemcpy(Lh->b, b, size_t(Lh->n_out) * 4, k));
+  p->legacy_dirty = true;
   return PT_OK;
 }
 
