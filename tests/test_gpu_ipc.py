@@ -4,11 +4,8 @@ neighbour's memory). Here both handles live in one process on GPU 0 with 74 CTAs
 their persistent kernels run concurrently on disjoint SMs: results must equal the
 single-handle D=2 pipeline bit for bit.
 
-(Two processes sharing one GPU are time-sliced by the driver. Under time-slicing even two
-independent single-handle pipelines drift from a solo run (tools/timeslice_probe.py),
-while random stalls of up to 1 ms per warp leave them bitwise equal (PT_JITTER). So that
-setup is not a parity test; DESIGN.md §5. Multi-GPU runs have one process per GPU and no
-time-slicing.)"""
+(The two-process version, one stage per process as in a multi-GPU job, is
+tests/test_gpu_ipc_process.py.)"""
 
 import numpy as np
 import pytest
