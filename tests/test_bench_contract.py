@@ -38,3 +38,21 @@ def test_gpu_arm_line():
     assert out["e2e"]["h2d_bytes_per_step"] > 0 and out["e2e"]["d2h_bytes_per_step"] > 0
     assert out["gpu_launches"] > 0 and out["step_api"]["value"] > 0
     assert "workload" in out["config"]
+
+
+@pytest.mark.gpu
+def test_gpu_arm_two_ranks_one_device():
+    """The multi-GPU launch path (torchrun, one stage per rank, CUDA IPC exchange), with both
+    ranks on GPU 0 (PT_BENCH_ONE_DEVICE; time-sliced, so the number itself is meaningless):
+    rank 0 prints one line for the whole job."""
+    env = dict(os.environ, PT_BENCH_ONE_DEVICE="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29531", os.path.join(ROOT, "bench.py"),
+           "--gpus", "2", "--steps", "2", "--warmup", "3", "--ticks", "8", "--no-extra"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    out = json.loads(lines[0])
+    assert out["n_gpus"] == 2 and out["config"]["parallelism"] == "pp2" and out["value"] > 0
+    assert out["latency"]["sample_latency_ticks"] == 2
