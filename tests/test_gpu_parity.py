@@ -431,3 +431,20 @@ def test_frozen_weights_output_equals_sequential(D):
 def test_concurrent_stages(D, counts):
     """Uniform widths: the local stages run concurrently on disjoint CTA ranges."""
     _case([128] * 9, counts, 40, 0.02)
+
+
+def test_empty_run_and_degenerate_widths():
+    """n = 0 ticks is a no-op; one-wide layers and a single output follow the oracle."""
+    m = mdl.mlp([1, 3, 1, 1], seed=2)
+    st = streams.SmoothStream(1, 1, seed=3)
+    xs, ys = st.block(0, 10)
+    p = engine.Pipeline(m, [2, 3], "sgd", 0.05, xs[0, 0], ys[0, 0])
+    o, l, v = p.run(xs[:0].astype(np.float32), ys[:0].astype(np.float32))
+    assert o.shape[0] == 0 and p.t == 0
+    p.close()
+    _case([1, 3, 1, 1], [2, 3], 10, 0.05)
+    _case([7, 1, 5], [2, 1], 10, 0.05, act="tanh")
+
+
+def test_softmax_ce_two_classes_batch1():
+    _case([9, 17, 2], [2, 1], 20, 0.05, loss="softmax_ce")
