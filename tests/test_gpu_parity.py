@@ -448,3 +448,10 @@ def test_empty_run_and_degenerate_widths():
 
 def test_softmax_ce_two_classes_batch1():
     _case([9, 17, 2], [2, 1], 20, 0.05, loss="softmax_ce")
+
+
+def test_microbatch_generic_small_lr():
+    """Generic tick path at micro-batch 16 with a small learning rate: the update sums the
+    batch's dW before one rounding of W (sixteen separate roundings lost small steps)."""
+    _case([128] * 4, [5], 13, 0.001, seed=830, M=16)
+    _case([66, 184, 244, 50, 16, 279], [2, 7], 13, 0.001, seed=830, M=16)
