@@ -912,6 +912,10 @@ int run_impl(pt_pipeline* p, const float* xs, const float* ys, int64_t n, float*
   P.Fy = Fy;
   P.b1 = 0.9f;  // Adam (oracle/netcore.py Adam)
   P.b2 = 0.999f;
+  P.b1d = 0.9;
+  P.b2d = 0.999;
+  P.omb1 = float(1.0 - 0.9);
+  P.omb2 = float(1.0 - 0.999);
   P.eps = 1e-8f;
   P.xs = first ? p->xs_pad : nullptr;
   P.ys = ys_dev;

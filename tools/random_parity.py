@@ -13,6 +13,8 @@ def random_case(rng):
     M = int(rng.choice([1, 1, 2, 4, 16]))
     if M == 16 and rng.random() < 0.5:
         widths = [256 * int(rng.integers(1, 3)) for _ in range(L + 1)]  # the tile kernel
+    elif rng.random() < 0.3:
+        widths = [int(rng.integers(1, 300))] * (L + 1)  # uniform: concurrent local stages
     n_layers = 2 * L - 1  # dense + act pairs, linear head
     D = int(rng.integers(1, min(L, 4) + 1))
     cuts = sorted(rng.choice(np.arange(1, L), D - 1, replace=False).tolist()) if D > 1 else []
