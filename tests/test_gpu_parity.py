@@ -455,3 +455,14 @@ def test_microbatch_generic_small_lr():
     batch's dW before one rounding of W (sixteen separate roundings lost small steps)."""
     _case([128] * 4, [5], 13, 0.001, seed=830, M=16)
     _case([66, 184, 244, 50, 16, 279], [2, 7], 13, 0.001, seed=830, M=16)
+
+
+def test_randomised_sweep():
+    """40 random configurations (tools/random_parity.py, seed 4): widths 1-300 incl. uniform
+    (concurrent stages) and tile shapes, depth, split, act, act_delay, batch, SGD/Adam, MSE/CE."""
+    from tools.random_parity import random_case
+    rng = np.random.default_rng(4)
+    for _ in range(40):
+        c = random_case(rng)
+        _case(c["widths"], c["counts"], c["T"], c["lr"], act=c["act"], seed=c["seed"], act_delay=c["act_delay"],
+              M=c["M"], optimizer=c["optimizer"], loss=c["loss"])
