@@ -12,7 +12,8 @@ import numpy as np  # noqa: E402
 from paper_2210_09147_b200 import engine, model as mdl, streams  # noqa: E402
 
 CASES = {"tile": ([256, 512, 512, 256, 256], 16), "tick": ([32, 64, 64, 64, 16], 1),
-         "tick_mb": ([64, 96, 96, 96, 32], 4), "tick_conc": ([256] * 9, 1), "tick_conc_mb": ([128] * 9, 4)}
+         "tick_mb": ([64, 96, 96, 96, 32], 4), "tick_conc": ([256] * 9, 1), "tick_conc_mb": ([128] * 9, 4),
+         "tick_mb_wide": ([1218, 3805, 2590, 1500], 2)}
 
 
 def main(kind, counts, learn):

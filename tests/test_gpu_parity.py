@@ -463,6 +463,14 @@ def test_randomised_sweep():
     from tools.random_parity import random_case
     rng = np.random.default_rng(4)
     for _ in range(40):
-        c = random_case(rng)
+        c = random_case(rng, 300)
         _case(c["widths"], c["counts"], c["T"], c["lr"], act=c["act"], seed=c["seed"], act_delay=c["act_delay"],
               M=c["M"], optimizer=c["optimizer"], loss=c["loss"])
+
+
+@pytest.mark.parametrize("M,act_delay", [(2, 0), (4, 1)])
+def test_generic_multichunk_partials(M, act_delay):
+    """Generic (batch > 1) path with wide layers, so a CTA streams several chunks per layer:
+    its g_in partial is a running sum over chunks and must carry the tick's tag only once
+    the last chunk is in (earlier running sums were readable too soon)."""
+    _case([1218, 3805, 2590, 1500], [2, 2, 1], 10, 0.05, act_delay=act_delay, M=M)

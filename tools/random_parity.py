@@ -7,14 +7,18 @@ import numpy as np
 from tests.test_gpu_parity import _case
 
 
-def random_case(rng):
+WMAX = int(os.environ.get("WMAX", "300"))
+
+
+def random_case(rng, wmax=None):
+    wmax = wmax or WMAX
     L = int(rng.integers(1, 6))
-    widths = [int(rng.integers(1, 300)) for _ in range(L + 1)]
+    widths = [int(rng.integers(1, wmax)) for _ in range(L + 1)]
     M = int(rng.choice([1, 1, 2, 4, 16]))
     if M == 16 and rng.random() < 0.5:
         widths = [256 * int(rng.integers(1, 3)) for _ in range(L + 1)]  # the tile kernel
     elif rng.random() < 0.3:
-        widths = [int(rng.integers(1, 300))] * (L + 1)  # uniform: concurrent local stages
+        widths = [int(rng.integers(1, wmax))] * (L + 1)  # uniform: concurrent local stages
     n_layers = 2 * L - 1  # dense + act pairs, linear head
     D = int(rng.integers(1, min(L, 4) + 1))
     cuts = sorted(rng.choice(np.arange(1, L), D - 1, replace=False).tolist()) if D > 1 else []
@@ -31,7 +35,7 @@ def random_case(rng):
 
 
 if __name__ == "__main__":
-    rng = np.random.default_rng(int(os.environ.get("SEED", "0")))
+    rng = np.random.default_rng(int(os.environ.get("SEED", "0")))  # WMAX=4096: large shapes
     n, bad = int(os.environ.get("N", "40")), 0
     for k in range(n):
         c = random_case(rng)
