@@ -15,7 +15,10 @@ def random_case(rng, wmax=None):
     L = int(rng.integers(1, 6))
     widths = [int(rng.integers(1, wmax)) for _ in range(L + 1)]
     M = int(rng.choice([1, 1, 2, 4, 16]))
-    if M == 16 and rng.random() < 0.5:
+    if os.environ.get("TILE_ONLY"):
+        M = 16
+        widths = [256 * int(rng.integers(1, 17)) for _ in range(L + 1)]  # the tile kernel, up to 4096
+    elif M == 16 and rng.random() < 0.5:
         widths = [256 * int(rng.integers(1, 3)) for _ in range(L + 1)]  # the tile kernel
     elif rng.random() < 0.3:
         widths = [int(rng.integers(1, wmax))] * (L + 1)  # uniform: concurrent local stages
@@ -31,7 +34,7 @@ def random_case(rng, wmax=None):
     loss = "softmax_ce" if rng.random() < 0.3 and widths[-1] >= 2 else "mse"
     return dict(widths=widths, counts=counts, T=int(rng.integers(2 * D + 2, 24)), lr=float(rng.choice([0.0, 0.01, 0.05])),
                 act=str(rng.choice(["relu", "tanh"])), act_delay=int(rng.integers(0, 2)), M=M,
-                optimizer=str(rng.choice(["sgd", "sgd", "adam"])), loss=loss, seed=int(rng.integers(0, 1000)))
+                optimizer=("sgd" if os.environ.get("TILE_ONLY") else str(rng.choice(["sgd", "sgd", "adam"]))), loss=loss, seed=int(rng.integers(0, 1000)))
 
 
 if __name__ == "__main__":
