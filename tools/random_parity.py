@@ -12,7 +12,7 @@ WMAX = int(os.environ.get("WMAX", "300"))
 
 def random_case(rng, wmax=None):
     wmax = wmax or WMAX
-    L = int(rng.integers(1, 6))
+    L = int(rng.integers(1, int(os.environ.get("LMAX", "5")) + 1))
     widths = [int(rng.integers(1, wmax)) for _ in range(L + 1)]
     M = int(rng.choice([1, 1, 2, 4, 16]))
     if os.environ.get("TILE_ONLY"):
@@ -23,7 +23,7 @@ def random_case(rng, wmax=None):
     elif rng.random() < 0.3:
         widths = [int(rng.integers(1, wmax))] * (L + 1)  # uniform: concurrent local stages
     n_layers = 2 * L - 1  # dense + act pairs, linear head
-    D = int(rng.integers(1, min(L, 4) + 1))
+    D = int(rng.integers(1, min(L, int(os.environ.get("DMAX", "4"))) + 1))
     cuts = sorted(rng.choice(np.arange(1, L), D - 1, replace=False).tolist()) if D > 1 else []
     units = np.diff([0] + cuts + [L]).tolist()
     counts, u = [], 0
