@@ -34,7 +34,8 @@ def random_case(rng, wmax=None):
     loss = "softmax_ce" if rng.random() < 0.3 and widths[-1] >= 2 else "mse"
     return dict(widths=widths, counts=counts, T=int(rng.integers(2 * D + 2, 24)), lr=float(rng.choice([0.0, 0.01, 0.05])),
                 act=str(rng.choice(["relu", "tanh"])), act_delay=int(rng.integers(0, 2)), M=M,
-                optimizer=("sgd" if os.environ.get("TILE_ONLY") else str(rng.choice(["sgd", "sgd", "adam"]))), loss=loss, seed=int(rng.integers(0, 1000)))
+                optimizer=("sgd" if os.environ.get("TILE_ONLY") else str(rng.choice(["sgd", "sgd", "adam"]))), loss=loss, seed=int(rng.integers(0, 1000)),
+                learn=bool(rng.random() >= float(os.environ.get("P_INFER", "0"))))
 
 
 if __name__ == "__main__":
@@ -44,7 +45,7 @@ if __name__ == "__main__":
         c = random_case(rng)
         try:
             _case(c["widths"], c["counts"], c["T"], c["lr"], act=c["act"], seed=c["seed"], act_delay=c["act_delay"],
-                  M=c["M"], optimizer=c["optimizer"], loss=c["loss"])
+                  M=c["M"], optimizer=c["optimizer"], loss=c["loss"], learn=c["learn"])
         except Exception as e:  # noqa: BLE001
             bad += 1
             print(f"case {k} FAILED {c}: {type(e).__name__}: {str(e)[:200]}", flush=True)
