@@ -6,7 +6,8 @@
  *     pipeline_run / pipeline_extract_weights;
  *   - paper API (reference PAPER.md:640-672): partime.pipeline.Pipeline(...).forward(inp, target).
  * Each entry point below names the reference operation it replaces. The Python
- * mirror (paper_2210_09147_b200.pipestream / .partime) binds this header through ctypes
+ * mirrors (the `pipestream` package = paper_2210_09147_b200.engine and friends, and the
+ * `partime` package = paper_2210_09147_b200.partime) bind this header through ctypes
  * (see INTEGRATION.md).
  *
  * Conventions
@@ -54,10 +55,12 @@ extern "C" {
 #define PT_ACT_TANH 2
 
 #define PT_LOSS_MSE 0        /* mean over M*F elements */
-#define PT_LOSS_SOFTMAX_CE 1 /* reserved: PT_EUNSUPPORTED on this path */
+#define PT_LOSS_SOFTMAX_CE 1 /* mean over M of -log softmax[target]; y holds one
+                                class index per sample; a target outside [0, F) -> PT_EINVAL */
 
 #define PT_OPT_SGD 0
-#define PT_OPT_ADAM 1        /* reserved: PT_EUNSUPPORTED on this path */
+#define PT_OPT_ADAM 1        /* beta = (0.9, 0.999), eps = 1e-8; the step count
+                                starts at the stage's warm-up gate t >= 2D-h-1 */
 
 typedef struct pt_pipeline pt_pipeline;
 
@@ -69,7 +72,7 @@ typedef struct pt_config {
   const int32_t* act;                /* L activations (PT_ACT_*) */
   int32_t loss;                      /* PT_LOSS_* */
   int32_t optimizer;                 /* PT_OPT_* */
-  float lr;                          /* learning rate (SGD step size) */
+  float lr;                          /* learning rate (SGD / Adam step size) */
   int32_t n_stages;                  /* D */
   const int32_t* stage_first_layer;  /* D+1 layer indices; [0] = 0, [D] = L (StagePlan) */
   int32_t batch;                     /* M rows per tick (1..16) */
@@ -93,7 +96,8 @@ int pt_set_params(pt_pipeline* p, int32_t layer, const float* W, const float* b,
 int pt_get_params(pt_pipeline* p, int32_t layer, float* W, float* b, int32_t where);
 
 /* pipeline_step / Pipeline.forward: one tick, synchronous.
- * x: [M, dims[0]] (needed iff stage 1 is local), y: [M, F] target of the SAME tick
+ * x: [M, dims[0]] (needed iff stage 1 is local), y: [M, F] (MSE) or [M] class indices
+ * (softmax-CE) target of the SAME tick
  * (queued internally for D-1 ticks). out: [M, F] output of sample t-(D-1),
  * loss: scalar (NaN when invalid), valid: t >= D-1. Any of out/loss/valid may be NULL. */
 int pt_step(pt_pipeline* p, const float* x, const float* y, float* out, float* loss,

@@ -171,6 +171,7 @@ struct pt_pipeline {
   }
   int* d_status = nullptr;
   long long* d_first_bad = nullptr;
+  long long* d_bad_target = nullptr;
   float* xs_pad = nullptr;
   size_t xs_cap = 0;  // ticks
   float* ys_stage = nullptr;
@@ -741,8 +742,10 @@ int create_impl(const pt_config* c, pt_pipeline* p) {
   PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&p->d_tick_end), sizeof(u64)));
   PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&p->d_status), sizeof(int)));
   PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&p->d_first_bad), sizeof(long long)));
+  PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&p->d_bad_target), sizeof(long long)));
   const long long big = std::numeric_limits<long long>::max();
   CUDA_TRY(cudaMemcpy(p->d_first_bad, &big, sizeof(big), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(p->d_bad_target, &big, sizeof(big), cudaMemcpyHostToDevice));
   p->yh = std::max(1, p->D);
   if (p->has_last()) PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&p->yhist), size_t(p->yh) * p->M * p->Fy() * 4));
   CUDA_TRY(cudaStreamCreateWithFlags(&p->own_stream, cudaStreamNonBlocking));
@@ -793,8 +796,15 @@ int read_status(pt_pipeline* p) {
     p->broken = true;
     return fail(PT_ETIMEOUT, "a stage waited longer than timeout_ms for a neighbour; pipeline state is lost");
   }
-  if (bad != std::numeric_limits<long long>::max()) {
-    const long long big = std::numeric_limits<long long>::max();
+  long long badt = std::numeric_limits<long long>::max();
+  CUDA_TRY(cudaMemcpy(&badt, p->d_bad_target, sizeof(long long), cudaMemcpyDeviceToHost));
+  const long long big = std::numeric_limits<long long>::max();
+  if (badt != big) {
+    CUDA_TRY(cudaMemcpy(p->d_bad_target, &big, sizeof(big), cudaMemcpyHostToDevice));
+    p->legacy_dirty = true;
+    return fail(PT_EINVAL, "target out of class range for cross-entropy (sample " + std::to_string(badt) + ")");
+  }
+  if (bad != big) {
     CUDA_TRY(cudaMemcpy(p->d_first_bad, &big, sizeof(big), cudaMemcpyHostToDevice));
     p->legacy_dirty = true;
     return fail(PT_ENONFINITE, "non-finite loss at step " + std::to_string(bad));
@@ -927,6 +937,7 @@ int run_impl(pt_pipeline* p, const float* xs, const float* ys, int64_t n, float*
   P.n = int(n);
   P.tick_end = p->d_tick_end;
   P.status = p->d_status;
+  P.bad_target = p->d_bad_target;
   P.timeout_ns = p->timeout_ns;
   P.nslot = p->nslot;
   P.slot_floats = p->slot_floats;

@@ -24,7 +24,8 @@
 // Warp roles: warp 0 = TMA producer (runs ahead across steps and ticks, stores updated
 // tiles back), warp 1 = MMA issuer (one thread), warps 2..9 = SIMT (split, operand
 // staging, TMEM epilogue, update, finalize, grid barrier).
-// Single process, every stage on this GPU (the multi-GPU path is pt::tick_kernel).
+// Stages may live on other GPUs/processes: their plain fp32 slots sit in an IPC-exported
+// tile comm block (TileComm) with tick counters (see partime_capi.cu).
 #pragma once
 #include "pt_kernels.cuh"
 #include "pt_tc.cuh"

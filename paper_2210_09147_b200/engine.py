@@ -21,7 +21,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib
-from .model import Model, StagePlan, fuse, plan_to_units
+from .model import Model, StagePlan, canonical_loss, fuse, plan_to_units
 
 try:  # torch is optional for the numpy API; required for device tensors
     import torch
@@ -101,6 +101,7 @@ class Pipeline:
                 where = f"stage boundary {h - 1}->{h}" if j == sfl[h - 1] else f"inside stage {h}"
                 raise ValueError(f"shape inference failed {where}: layer {units[j][0]} expects "
                                  f"{dense[j].in_dim}, receives {dims[j]} (SPEC.md:212)")
+        model.loss = canonical_loss(model.loss)
         if model.loss not in _lib.PT_LOSS:
             raise ValueError(f"unknown loss {model.loss!r}")
         if optimizer not in _lib.PT_OPT:
@@ -220,6 +221,8 @@ class Pipeline:
             raise ValueError(f"x_t has shape {tuple(x.shape)}, expected [{M}, {self.dims[0]}]")
         if y is not None and int(np.prod(tuple(y.shape))) != M * self.Fy:
             raise ValueError(f"target_t has shape {tuple(y.shape)}, expected [{M}, {self.Fy}]")
+        if y is not None and not dev:
+            self._check_targets(y, f"step {self._t}")
         if dev:
             out = torch.empty((M, F), dtype=torch.float32, device=x.device if x is not None else y.device)
             loss = torch.empty(1, dtype=torch.float32, device=out.device)
@@ -255,6 +258,8 @@ class Pipeline:
         dev = _is_cuda(xs) or _is_cuda(ys) or (xs is None and ys is None and torch is not None)
         xs = None if xs is None else _f32(xs)
         ys = None if ys is None else _f32(ys)
+        if ys is not None and not dev:
+            self._check_targets(ys, f"steps [{self._t}, {self._t + n})")
         if dev:
             d = xs.device if xs is not None else (ys.device if ys is not None else
                                                    torch.device("cuda", torch.cuda.current_device()))
@@ -278,7 +283,30 @@ class Pipeline:
         t0 = self._t
         self._t += n
         _lib.check(rc, f"pipeline_run at steps [{t0}, {t0 + n})")
+        if not has_last:
+            # this process does not own stage D: no outputs or losses here, but validity is
+            # known from the tick alone
+            ticks = np.arange(t0, t0 + n)
+            if dev:
+                valid.copy_(torch.from_numpy((ticks >= self.D - 1).astype(np.uint8)))
+                losses.fill_(float("nan"))
+                outs.fill_(float("nan"))
+            else:
+                valid[:] = ticks >= self.D - 1
+                losses[:] = np.nan
+                outs[:] = np.nan
         return outs, losses, valid
+
+    def _check_targets(self, y, where):
+        """softmax-CE targets are class indices in [0, F). Host arrays are
+        checked here; device targets are checked by the kernel (PT_EINVAL at sync)."""
+        if self.model.loss != "softmax_ce":
+            return
+        y = np.asarray(y)
+        bad = ~((y >= 0) & (y < self.F) & (y == np.floor(y)))
+        if bad.any():
+            raise ValueError(f"target out of class range for cross-entropy at {where}: "
+                             f"{y.reshape(-1)[np.argmax(bad.reshape(-1))]!r} not in [0, {self.F})")
 
     def sync(self):
         _lib.check(self._lib.pt_sync(self._h), "sync")
@@ -381,7 +409,14 @@ def pipeline_run(pipeline, stream, n_steps, log_sink=None, chunk=256):
     while done < n_steps:
         n = min(chunk, n_steps - done)
         if hasattr(stream, "block"):
-            xs, ys = stream.block(getattr(stream, "t", done), n)
+            t_s = getattr(stream, "t", done)
+            if hasattr(stream, "__len__"):
+                # finite stream (replay over a DatasetFile): stop cleanly at its end with a
+                # partial report
+                n = min(n, len(stream) - t_s)
+                if n <= 0:
+                    break
+            xs, ys = stream.block(t_s, n)
             if hasattr(stream, "t"):
                 stream.t += n
         else:
@@ -407,11 +442,11 @@ def pipeline_run(pipeline, stream, n_steps, log_sink=None, chunk=256):
             v = bool(valid[i])
             rep.steps.append(t)
             rep.sample_ids.append(t - (pipeline.D - 1))
-            rep.losses.append(float(losses[i]) if v else None)
+            rep.losses.append(float(losses[i]) if (v and np.isfinite(losses[i])) else None)
             rep.valid.append(v)
             rep.step_wall_seconds.append(dt)
         done += n
-        if n < chunk and not hasattr(stream, "block"):
+        if n < chunk and (not hasattr(stream, "block") or hasattr(stream, "__len__")):
             break
     rep.elapsed = time.perf_counter() - t_start
     rep.outputs = np.concatenate(outs_all) if outs_all else None

@@ -19,6 +19,12 @@ import numpy as np
 
 SUPPORTED = ("dense", "relu", "tanh")
 REFERENCE_ONLY = ("conv2d", "avgpool2d", "flatten", "residual_add")
+# SPEC.md:74-75 names the loss "softmax_cross_entropy"; "softmax_ce" is the short form
+LOSS_ALIASES = {"softmax_cross_entropy": "softmax_ce"}
+
+
+def canonical_loss(name):
+    return LOSS_ALIASES.get(name, name)
 
 
 @dataclass
@@ -38,6 +44,9 @@ class Model:
     loss: str = "mse"
     input_shape: tuple = ()
     output_dim: int = 0
+
+    def __post_init__(self):
+        self.loss = canonical_loss(self.loss)
 
     @property
     def dense_layers(self):

@@ -18,9 +18,13 @@ def sequential_to_model(net, loss="mse"):
     layers = []
     for i, mod in enumerate(net):
         if isinstance(mod, nn.Linear):
+            if mod.bias is None:
+                # the kernels train every layer's bias; a zero bias would be trained and then
+                # dropped by sync_to_net, so the synced net would not reproduce the pipeline
+                raise NotImplementedError(f"module {i}: nn.Linear(bias=False) is not supported on the B200 "
+                                          "path (every dense layer trains a bias)")
             W = mod.weight.detach().float().cpu().numpy().copy()
-            b = (mod.bias.detach().float().cpu().numpy().copy() if mod.bias is not None
-                 else np.zeros(mod.out_features, np.float32))
+            b = mod.bias.detach().float().cpu().numpy().copy()
             layers.append(LayerSpec("dense", mod.in_features, mod.out_features, W=W, b=b))
         elif isinstance(mod, nn.ReLU):
             layers.append(LayerSpec("relu"))

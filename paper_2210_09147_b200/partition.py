@@ -23,6 +23,8 @@ import time
 from dataclasses import dataclass, field
 from functools import lru_cache
 
+from .model import canonical_loss
+
 
 def balance(costs, D, transfer=None):
     """Layer counts of the min-max contiguous split of `costs` into D blocks.
@@ -187,7 +189,7 @@ def profile_costs(model, sample_input, iters=5, warmup_iters=2, device=0):
     try:
       with torch.cuda.device(device):
         xs = np.tile(si.reshape(1, M, -1), (T, 1, 1)).astype(np.float32)
-        ys = np.zeros((T, M, 1 if model.loss == "softmax_ce" else dims[-1]), np.float32)
+        ys = np.zeros((T, M, 1 if canonical_loss(model.loss) == "softmax_ce" else dims[-1]), np.float32)
         if M == 1:
             xs, ys = xs[:, 0], ys[:, 0]
         p = Pipeline(model, [len(model.layers)], "sgd", 1e-9, si, ys[0])
