@@ -61,7 +61,8 @@ __global__ void __launch_bounds__(288, 1) step_kernel(const __grid_constant__ Ar
   float* act = reinterpret_cast<float*>(sm + ring_bytes);  // [WD] F: input vector
   float* red = act + WD;                                     // [NCW][NRM]
   float* dlt = red + 16 * NRM;                               // [NRM] B: own delta
-  uint64_t* full = reinterpret_cast<uint64_t*>(dlt + NRM);
+  float* pl = dlt + NRM;                                     // [NRM][NCT] F: per-lane row partials
+  uint64_t* full = reinterpret_cast<uint64_t*>(pl + NRM * NCT);
   uint64_t* empty = full + A.nslot;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, G = gridDim.x, c = blockIdx.x;
   const int r0 = int((long long)WD * c / G), r1 = int((long long)WD * (c + 1) / G), nrows = r1 - r0;
@@ -116,17 +117,27 @@ __global__ void __launch_bounds__(288, 1) step_kernel(const __grid_constant__ Ar
     // kind 2 = tick: 32 F steps (read + write back) then 32 B steps (read only)
     const bool kindF = A.kind == K_F || (A.kind == 2 && (s % 64) < 32);
     // ---------------------------------------------------------------- dependency
-    if (A.supply != S_NODEP && s > 0) {
+    const bool prevF = A.kind == 2 ? ((s + 63) % 64) < 32 : kindF;  // tick mode: the step before
+    if (A.supply != S_NODEP && s > 0 && prevF == kindF) {
       if (kindF) {
         // all-gather: every thread issues its 4 pair loads, then checks
         const u64* src = A.vec + size_t(s & 3) * G * G * NRM;
         u64 v[8];
 #pragma unroll
         for (int k = 0; k < 4; ++k) ld2_tv_gpu(src + tid * 2 + k * 512, v[2 * k], v[2 * k + 1]);
+        // re-poll every stale pair together: one round trip per round, not one per pair
+        for (;;) {
+          bool stale = false;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) stale |= tv_tag(v[2 * k]) != tag || tv_tag(v[2 * k + 1]) != tag;
+          if (!stale) break;
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (tv_tag(v[2 * k]) != tag || tv_tag(v[2 * k + 1]) != tag)
+              ld2_tv_gpu(src + tid * 2 + k * 512, v[2 * k], v[2 * k + 1]);
+        }
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          while (tv_tag(v[2 * k]) != tag || tv_tag(v[2 * k + 1]) != tag)
-            ld2_tv_gpu(src + tid * 2 + k * 512, v[2 * k], v[2 * k + 1]);
           act[tid * 2 + k * 512] = tv_val(v[2 * k]) * 1e-3f + 1.f;
           act[tid * 2 + k * 512 + 1] = tv_val(v[2 * k + 1]) * 1e-3f + 1.f;
         }
@@ -143,12 +154,17 @@ __global__ void __launch_bounds__(288, 1) step_kernel(const __grid_constant__ Ar
             const int pc = grp + 16 * j;
             v[j] = pc < G ? ld_tv_gpu(src + size_t(pc) * NRM + row) : pack_tv(0.f, tag);
           }
+          for (;;) {
+            bool stale = false;
 #pragma unroll
-          for (int j = 0; j < 10; ++j) {
-            const int pc = grp + 16 * j;
-            while (tv_tag(v[j]) != tag) v[j] = ld_tv_gpu(src + size_t(pc) * NRM + row);
-            sum += tv_val(v[j]);
+            for (int j = 0; j < 10; ++j) stale |= tv_tag(v[j]) != tag;
+            if (!stale) break;
+#pragma unroll
+            for (int j = 0; j < 10; ++j)
+              if (tv_tag(v[j]) != tag) v[j] = ld_tv_gpu(src + size_t(grp + 16 * j) * NRM + row);
           }
+#pragma unroll
+          for (int j = 0; j < 10; ++j) sum += tv_val(v[j]);
         }
         red[grp * NRM + row] = sum;
         cons_sync(NCT);
@@ -158,7 +174,7 @@ __global__ void __launch_bounds__(288, 1) step_kernel(const __grid_constant__ Ar
           dlt[tid] = d * 1e-3f + 1.f;
         }
       }
-    } else if (s == 0) {
+    } else if (s == 0 || prevF != kindF) {
       for (int j = tid; j < WD; j += NCT) act[j] = 1.f;
       if (tid < NRM) dlt[tid] = 1.f;
     }
@@ -179,34 +195,18 @@ __global__ void __launch_bounds__(288, 1) step_kernel(const __grid_constant__ Ar
         wb = reinterpret_cast<const float*>(sm + size_t(slot) * A.slot_bytes);
       }
       if (kindF) {
-        float p[4];
-#pragma unroll
-        for (int r = 0; r < 4; ++r)
-          p[r] = r < nr ? dot4(lds4(wb + r * WD + c0), a0) + dot4(lds4(wb + r * WD + c0 + 128), a1) : 0.f;
-        // 4 row partials -> lane l holds row (l & 3) of this warp (6 shuffles)
-        {
-          const bool up2 = lane & 2, up1 = lane & 1;
-          float s0 = up2 ? p[0] : p[2], k0v = up2 ? p[2] : p[0];
-          float s1 = up2 ? p[1] : p[3], k1v = up2 ? p[3] : p[1];
-          float q0 = k0v + __shfl_xor_sync(0xffffffffu, s0, 2);
-          float q1 = k1v + __shfl_xor_sync(0xffffffffu, s1, 2);
-          float sd = up1 ? q0 : q1, kp = up1 ? q1 : q0;
-          float v = kp + __shfl_xor_sync(0xffffffffu, sd, 1);
-          v += __shfl_xor_sync(0xffffffffu, v, 4);
-          v += __shfl_xor_sync(0xffffffffu, v, 8);
-          v += __shfl_xor_sync(0xffffffffu, v, 16);
-          // lane bits (1,0) -> row index: bit1 selected p[2]/p[3] half, bit0 the odd row
-          if (lane < 4 && lane < nr) red[warp * NRM + k0 + lane] = v;
-        }
+        // per-lane row partials go to smem [row][warp][lane]; reduced once per step
+        for (int r = 0; r < nr; ++r)
+          pl[(k0 + r) * NCT + tid] = dot4(lds4(wb + r * WD + c0), a0) + dot4(lds4(wb + r * WD + c0 + 128), a1);
       } else {
-#pragma unroll
-        for (int r = 0; r < 4; ++r)
-          if (r < nr) {
+        for (int r = 0; r < nr; ++r) {
+          {
             const float d = dlt[k0 + r];
             const float4 w0 = lds4(wb + r * WD + c0), w1 = lds4(wb + r * WD + c0 + 128);
             g0.x = fmaf(w0.x, d, g0.x); g0.y = fmaf(w0.y, d, g0.y); g0.z = fmaf(w0.z, d, g0.z); g0.w = fmaf(w0.w, d, g0.w);
             g1.x = fmaf(w1.x, d, g1.x); g1.y = fmaf(w1.y, d, g1.y); g1.z = fmaf(w1.z, d, g1.z); g1.w = fmaf(w1.w, d, g1.w);
           }
+        }
       }
       if (!resident) {
         __syncwarp();
@@ -218,10 +218,16 @@ __global__ void __launch_bounds__(288, 1) step_kernel(const __grid_constant__ Ar
     // ---------------------------------------------------------------- publish
     if (kindF) {
       cons_sync(NCT);
-      if (tid < nrows) {
+      for (int rr = warp; rr < nrows; rr += NCW) {
         float z = 0.f;
 #pragma unroll
-        for (int w = 0; w < NCW; ++w) z += red[w * NRM + tid];
+        for (int j = 0; j < 8; ++j) z += pl[rr * NCT + lane + 32 * j];
+        z = warp_sum(z);
+        if (lane == 0) red[rr] = z;
+      }
+      cons_sync(NCT);
+      if (tid < nrows) {
+        const float z = red[tid];
         st_tv_gpu(A.vec + size_t((s + 1) & 3) * G * G * NRM + r0 + tid, pack_tv(z, tag + 1));
       }
     } else {
@@ -273,7 +279,7 @@ int main(int argc, char** argv) {
     A.steps = steps;
     A.ev = ev;
     A.nev = nev;
-    const size_t smem = size_t(nslot) * A.slot_bytes + (WD + 16 * NRM + NRM) * 4 + 2 * nslot * 8 + 64;
+    const size_t smem = size_t(nslot) * A.slot_bytes + (WD + 16 * NRM + NRM + NRM * NCT) * 4 + 2 * nslot * 8 + 64;
     if (smem > 227 * 1024) return;
     cudaFuncSetAttribute(step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     float best = 1e9;
