@@ -22,6 +22,7 @@
 #include "partime_b200.h"
 #include "pt_kernels.cuh"
 #include "pt_tile.cuh"
+#include "pt_panel.cuh"
 
 using pt::u64;
 
@@ -114,6 +115,13 @@ struct LayerHost {
   u64* part[2] = {nullptr, nullptr};
   int rows_per_chunk = 0;
   int cache_in = 0, cache_out = 0;
+  // batch-1 panel path (pt_panel.cuh): 16 x 16-tiled weights in two buffers, g_in vectors,
+  // delta store, and the tick of the last pt_set_params (discards the pending update)
+  int R = 0, C = 0;
+  float* Wt[2] = {nullptr, nullptr};
+  u64* gin[2] = {nullptr, nullptr};
+  u64* dst = nullptr;
+  long long set_tick = 0;
 };
 
 struct StageHost {
@@ -205,6 +213,15 @@ struct pt_pipeline {
   int nslot = 0, slot_floats = 0, qw = 0, act_off = 0, spart_off = 0, spart_floats = 0, delta_off = 0,
       red_off = 0, scal_off = 0, bar_off = 0, flags_off = 0, desc_off = 0, bias_off = 0, smem_bytes = 0;
   int dbg = 0;                                        // diagnostics (env PT_DBG)
+  // batch-1 panel path (pt_panel.cuh): M == 1, SGD
+  bool panel = false;
+  pt::PLayer* d_players = nullptr;
+  pt::PStage* d_pstages = nullptr;
+  CUtensorMap* d_pmaps = nullptr;
+  float* rowbuf = nullptr;  // row-major staging of pt_set_params / pt_get_params
+  size_t rowbuf_floats = 0;
+  int pn_nslot = 0, pn_va = 0, pn_vb = 0, pn_sown = 0, pn_sah = 0, pn_red = 0, pn_bar = 0, pn_desc = 0, pn_bias = 0,
+      pn_smem = 0, pn_pf = 8;
   // micro-batch tensor-core path (pt_tile.cuh): M == 16, widths % 256 == 0, single process
   bool tile = false;
   int t_smem = 0, t_maxn = 0;
@@ -274,6 +291,8 @@ int ensure(pt_pipeline* p, T** buf, size_t* cap, size_t need, size_t elems_per) 
   return PT_OK;
 }
 
+int upload_panel_desc(pt_pipeline* p);
+
 int upload_desc(pt_pipeline* p) {
   std::vector<pt::LayerDev> ld(p->layers.size());
   for (size_t i = 0; i < p->layers.size(); ++i) {
@@ -335,6 +354,7 @@ int upload_desc(pt_pipeline* p) {
   CUDA_TRY(cudaMemcpy(p->d_layers, ld.data(), ld.size() * sizeof(pt::LayerDev), cudaMemcpyHostToDevice));
   CUDA_TRY(cudaMemcpy(p->d_stages, sd.data(), sd.size() * sizeof(pt::StageDev), cudaMemcpyHostToDevice));
   p->legacy_dirty = true;
+  if (p->panel) return upload_panel_desc(p);
   return PT_OK;
 }
 
@@ -562,6 +582,195 @@ int setup_tile(pt_pipeline* p) {
   return PT_OK;
 }
 
+
+// ---------------------------------------------------------------- panel path (pt_panel.cuh)
+// Descriptors of the panel kernel (rebuilt after pt_set_params and every IPC import).
+int upload_panel_desc(pt_pipeline* p) {
+  std::vector<pt::PLayer> pl(p->layers.size());
+  for (size_t i = 0; i < p->layers.size(); ++i) {
+    const LayerHost& h = p->layers[i];
+    pt::PLayer& d = pl[i];
+    memset(&d, 0, sizeof(d));
+    for (int j = 0; j < 2; ++j) {
+      d.W[j] = h.Wt[j] ? h.Wt[j] : h.Wt[0];
+      d.tm[j] = p->d_pmaps ? p->d_pmaps + 2 * i + j : nullptr;
+      d.gin[j] = h.gin[j];
+    }
+    d.b = h.b;
+    d.dst = h.dst;
+    if (h.dst) {
+      d.dsrc = h.dst;
+      d.dsrc_stride = h.R * pt::PN_TS;
+    } else if (i + 1 < p->layers.size()) {
+      d.dsrc = p->layers[i + 1].gin[0];
+      d.dsrc_stride = p->layers[i + 1].C * pt::PN_TS;
+    }
+    d.n_in = h.n_in;
+    d.n_out = h.n_out;
+    d.R = h.R;
+    d.C = h.C;
+    d.act = h.act;
+    d.cache_in = h.cache_in;
+    d.cache_out = h.cache_out;
+    d.set_tick = h.set_tick;
+  }
+  std::vector<pt::PStage> ps(p->stages.size());
+  for (size_t s = 0; s < p->stages.size(); ++s) {
+    const StageHost& h = p->stages[s];
+    const int s0 = h.h - 1;
+    pt::PStage& d = ps[s];
+    memset(&d, 0, sizeof(d));
+    d.h = h.h;
+    d.first = h.first_local;
+    d.k = h.k;
+    d.G_up = h.G_up;
+    d.G_down = h.G_down;
+    d.up_remote = h.up_remote ? 1 : 0;
+    d.down_remote = h.down_remote ? 1 : 0;
+    d.ld0 = h.ld0;
+    d.ldk = h.ldk;
+    for (int j = 0; j < 4; ++j) d.cache[j] = h.cache + size_t(j) * h.cache_words;
+    const CommLayout own = p->layout_of(s0);
+    for (int j = 0; j < 2; ++j) {
+      d.inslot[j] = reinterpret_cast<u64*>(h.comm + own.inslot(j));
+      d.gslot[j] = reinterpret_cast<u64*>(h.comm + own.gslot(j));
+    }
+    d.act_credit = reinterpret_cast<u64*>(h.comm + CommLayout::ACT_CREDIT);
+    d.g_credit = reinterpret_cast<u64*>(h.comm + CommLayout::G_CREDIT);
+    if (h.down) {
+      const CommLayout dn = p->layout_of(s0 + 1);
+      for (int j = 0; j < 2; ++j) d.peer_inslot[j] = reinterpret_cast<u64*>(h.down + dn.inslot(j));
+      d.peer_g_credit = reinterpret_cast<u64*>(h.down + CommLayout::G_CREDIT);
+    }
+    if (h.up) {
+      const CommLayout upl = p->layout_of(s0 - 1);
+      for (int j = 0; j < 2; ++j) d.peer_gslot[j] = reinterpret_cast<u64*>(h.up + upl.gslot(j));
+      d.peer_act_credit = reinterpret_cast<u64*>(h.up + CommLayout::ACT_CREDIT);
+    }
+  }
+  // stream-ordered: a pt_set_params between runs must not race the next launch's descriptor read
+  CUDA_TRY(cudaStreamSynchronize(p->stream));
+  CUDA_TRY(cudaMemcpy(p->d_players, pl.data(), pl.size() * sizeof(pt::PLayer), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(p->d_pstages, ps.data(), ps.size() * sizeof(pt::PStage), cudaMemcpyHostToDevice));
+  p->legacy_dirty = true;
+  return PT_OK;
+}
+
+// 3-D fp32 tensor map {256 floats, C, R} over tiled weights; box {256, 1, 32}: one column
+// panel piece of 32 tiles (rows beyond R are zero-filled). 0 = ok
+int panel_tmap(CUtensorMap* tm, const float* base, int R, int C) {
+  static pt::PFN_encodeTiled fn = nullptr;
+  if (fn == nullptr) {
+    void* q = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &q, cudaEnableDefault, &qr) != cudaSuccess || q == nullptr)
+      return -1;
+    fn = reinterpret_cast<pt::PFN_encodeTiled>(q);
+  }
+  const cuuint64_t dims[3] = {cuuint64_t(pt::PN_TILE), cuuint64_t(C), cuuint64_t(R)};
+  const cuuint64_t strides[2] = {cuuint64_t(pt::PN_TILE) * 4, cuuint64_t(C) * pt::PN_TILE * 4};
+  const cuuint32_t box[3] = {cuuint32_t(pt::PN_TILE), 1, cuuint32_t(pt::PN_CT)};
+  const cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : int(r);
+}
+
+// stage (1-based) owning global layer `layer`
+int stage_of_layer(const pt_pipeline* p, int layer) {
+  int h = 1;
+  while (h < p->D && layer >= p->sfl[h]) ++h;
+  return h;
+}
+
+// Buffers, tensor maps, shared-memory plan and descriptors of the panel path.
+int setup_panel(pt_pipeline* p) {
+  const int G = p->G;
+  int maxw = 16, maxrown = 16, maxcoln = 16;
+  size_t bias_rows = 0;
+  for (size_t i = 0; i < p->layers.size(); ++i) {
+    LayerHost& Lh = p->layers[i];
+    bias_rows += size_t((Lh.R + G - 1) / G) * pt::PN_TS;
+    maxw = std::max(maxw, std::max(Lh.R, Lh.C) * pt::PN_TS);
+    maxrown = std::max(maxrown, (Lh.R + G - 1) / G * pt::PN_TS);
+    maxcoln = std::max(maxcoln, (Lh.C + G - 1) / G * pt::PN_TS);
+    const int li_global = p->layer_base + int(i);
+    if (p->learn) {
+      // a stage's last layer keeps its own delta [2][R*16]; every other layer's delta is the next
+      // layer's published vector gin [2][C*16] (both tick parities in one block)
+      const int h = stage_of_layer(p, li_global);
+      if (li_global + 1 == p->sfl[h])
+        PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&Lh.dst), size_t(2) * Lh.R * pt::PN_TS * sizeof(u64)));
+      if (li_global != 0) {
+        PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&Lh.gin[0]), size_t(2) * Lh.C * pt::PN_TS * sizeof(u64)));
+        Lh.gin[1] = Lh.gin[0] + size_t(Lh.C) * pt::PN_TS;
+      }
+    }
+  }
+  if (p->learn) {
+    std::vector<CUtensorMap> maps(2 * p->layers.size());
+    for (size_t i = 0; i < p->layers.size(); ++i)
+      for (int j = 0; j < 2; ++j)
+        if (panel_tmap(&maps[2 * i + j], p->layers[i].Wt[j], p->layers[i].R, p->layers[i].C))
+          return fail(PT_ECUDA, "cuTensorMapEncodeTiled failed for layer " + std::to_string(p->layer_base + i));
+    PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&p->d_pmaps), maps.size() * sizeof(CUtensorMap)));
+    CUDA_TRY(cudaMemcpy(p->d_pmaps, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
+  }
+  PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&p->d_players), p->layers.size() * sizeof(pt::PLayer)));
+  PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&p->d_pstages), p->stages.size() * sizeof(pt::PStage)));
+  // shared memory: ring (32 KB slots) first, then the vectors and small buffers
+  auto a128 = [](size_t v) { return int(align_up(v, 128)); };
+  const int desc = a128(p->layers.size() * sizeof(pt::PLayer) + p->stages.size() * sizeof(pt::PStage) +
+                        p->layers.size() * sizeof(int));
+  const int bias = a128(bias_rows * 4);
+  const int tail = 2 * a128(size_t(maxw) * 4) + a128(size_t(maxrown) * 4) + a128(size_t(maxcoln) * 4) +
+                   a128((256 + 64) * 4) + a128(2 * pt::PN_MAXSLOT * 8) + desc + bias;
+  const int slot_bytes = pt::PN_SLOT_FLOATS * 4;
+  int nslot = std::min(pt::PN_MAXSLOT, (pt::SMEM_MAX - tail) / slot_bytes);
+  if (const char* e = getenv("PT_NSLOT")) nslot = std::min(nslot, std::max(2, atoi(e)));
+  if (nslot < 2)
+    return fail(PT_EINVAL, "shared memory too small for this layer shape (rows per CTA); use a larger grid");
+  p->pn_nslot = nslot;
+  int off = nslot * slot_bytes;
+  p->pn_va = off;
+  off += a128(size_t(maxw) * 4);
+  p->pn_vb = off;
+  off += a128(size_t(maxw) * 4);
+  p->pn_sown = off;
+  off += a128(size_t(maxrown) * 4);
+  p->pn_sah = off;
+  off += a128(size_t(maxcoln) * 4);
+  p->pn_red = off;
+  off += a128((256 + 64) * 4);
+  p->pn_bar = off;
+  off += a128(2 * pt::PN_MAXSLOT * 8);
+  p->pn_desc = off;
+  off += desc;
+  p->pn_bias = off;
+  off += bias;
+  p->pn_smem = off;
+  if (const char* e = getenv("PT_PF_CHUNKS")) p->pn_pf = std::max(0, atoi(e));
+  if (p->pn_smem > pt::SMEM_MAX) return fail(PT_EINVAL, "panel shared-memory plan exceeds 227 KB");
+  CUDA_TRY(cudaFuncSetAttribute(pt::panel_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, pt::SMEM_MAX));
+  return PT_OK;
+}
+
+// the weight buffer holding W^(t_next - 1) (before its pending update)
+int panel_cur(const pt_pipeline* p) { return p->learn ? int((p->t_next - 1) & 1) : 0; }
+
+int panel_rowbuf(pt_pipeline* p, size_t floats) {
+  if (p->rowbuf_floats >= floats && p->rowbuf) return PT_OK;
+  CUDA_TRY(cudaStreamSynchronize(p->stream));
+  dev_free(p, p->rowbuf);
+  p->rowbuf = nullptr;
+  PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&p->rowbuf), floats * 4));
+  CUDA_TRY(cudaStreamSynchronize(0));
+  p->rowbuf_floats = floats;
+  return PT_OK;
+}
+
+
 int create_impl(const pt_config* c, pt_pipeline* p) {
   std::string why;
   if (validate(c, &why) != PT_OK) return fail(PT_EINVAL, why);
@@ -617,6 +826,16 @@ int create_impl(const pt_config* c, pt_pipeline* p) {
       p->G = std::min(c->grid > 0 ? c->grid : sms, units);
     }
   }
+  {
+    // batch-1 panel path (pt_panel.cuh): SGD, any widths; stages in turn on every CTA.
+    // PT_PANEL=0 keeps the row-owned tick kernel.
+    bool ok = !p->tile && p->M == 1 && p->opt == PT_OPT_SGD;
+    if (const char* e = getenv("PT_PANEL")) ok = ok && atoi(e) != 0;
+    if (ok) {
+      p->panel = true;
+      p->G = c->grid > 0 ? c->grid : std::min(sms, 128);  // 2048-wide layers: one 16-row block per CTA
+    }
+  }
 
   // local layers
   const int s_lo = p->local_first, s_hi = p->local_first + p->local_count;
@@ -629,7 +848,15 @@ int create_impl(const pt_config* c, pt_pipeline* p) {
     Lh.ld_in = pad_dim(Lh.n_in);
     Lh.ld_out = pad_dim(Lh.n_out);
     Lh.act = p->act[l];
-    PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&Lh.W), size_t(Lh.n_out) * Lh.ld_in * 4));
+    Lh.R = (Lh.n_out + pt::PN_TS - 1) / pt::PN_TS;
+    Lh.C = (Lh.n_in + pt::PN_TS - 1) / pt::PN_TS;
+    if (p->panel) {
+      const size_t tiled = size_t(Lh.R) * Lh.C * pt::PN_TILE * 4;
+      PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&Lh.Wt[0]), tiled));
+      if (p->learn) PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&Lh.Wt[1]), tiled));
+    } else {
+      PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&Lh.W), size_t(Lh.n_out) * Lh.ld_in * 4));
+    }
     PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&Lh.b), size_t(Lh.n_out) * 4));
     if (p->opt == PT_OPT_ADAM && p->learn) {
       PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&Lh.mW), size_t(Lh.n_out) * Lh.ld_in * 4));
@@ -644,7 +871,7 @@ int create_impl(const pt_config* c, pt_pipeline* p) {
   // weight bytes, and exchange through L2 exactly as separate GPUs would through NVLink
   p->stage_cta0.assign(p->local_count, 0);
   p->stage_ncta.assign(p->local_count, p->G);
-  p->conc = p->local_count > 1 && !p->tile && p->G >= 2 * p->local_count;
+  p->conc = p->local_count > 1 && !p->tile && !p->panel && p->G >= 2 * p->local_count;
   // uniform widths only: with uneven layers (C5) a byte-proportional split leaves the stage
   // with the most lock-step steps per byte behind, measured slower than running in turn
   for (const LayerHost& Lh : p->layers)
@@ -688,8 +915,10 @@ int create_impl(const pt_config* c, pt_pipeline* p) {
       p->stage_ncta.assign(p->local_count, p->G);
     }
   }
-  PT_TRY(plan_smem(p));
-  for (LayerHost& Lh : p->layers) Lh.rows_per_chunk = p->slot_floats / Lh.ld_in;
+  if (!p->panel) {
+    PT_TRY(plan_smem(p));
+    for (LayerHost& Lh : p->layers) Lh.rows_per_chunk = p->slot_floats / Lh.ld_in;
+  }
   // local stages
   for (int s0 = s_lo; s0 < s_hi; ++s0) {
     StageHost S;
@@ -711,11 +940,13 @@ int create_impl(const pt_config* c, pt_pipeline* p) {
     }
     off += size_t(p->M) * p->layers[S.first_local + S.k - 1].ld_out;
     S.cache_words = align_up(off, 64);
-    PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&S.cache), 3 * S.cache_words * sizeof(u64)));
+    // cache slots: tick mod 3 (tick kernel) or mod 4 (panel kernel: a slot is read as the
+    // deferred update's a_hat up to two ticks after it was written)
+    PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&S.cache), (p->panel ? 4 : 3) * S.cache_words * sizeof(u64)));
     const CommLayout cl = p->layout_of(s0);
     PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&S.comm), cl.total));
     // g_in partials: needed by every layer except stage 1's first
-    if (p->learn && !p->tile) {
+    if (p->learn && !p->tile && !p->panel) {
       for (int i = 0; i < S.k; ++i) {
         if (S.h == 1 && i == 0) continue;
         LayerHost& Lh = p->layers[S.first_local + i];
@@ -753,6 +984,7 @@ int create_impl(const pt_config* c, pt_pipeline* p) {
   CUDA_TRY(cudaEventCreate(&p->ev0));
   CUDA_TRY(cudaEventCreate(&p->ev1));
   if (p->tile) PT_TRY(setup_tile(p));
+  if (p->panel) PT_TRY(setup_panel(p));
   PT_TRY(upload_desc(p));
   CUDA_TRY(cudaDeviceSynchronize());
   return PT_OK;
@@ -966,7 +1198,55 @@ int run_impl(pt_pipeline* p, const float* xs, const float* ys, int64_t n, float*
   if (const char* e = getenv("PT_JITTER_MASK")) P.jitter_mask = atoi(e);
   if (p->d_trace) CUDA_TRY(cudaMemsetAsync(p->d_trace, 0, size_t(p->trace_cap) * sizeof(u64), p->stream));
 
-  if (p->tile) {
+  if (p->panel) {
+    pt::PParams Q;
+    memset(&Q, 0, sizeof(Q));
+    Q.stages = p->d_pstages;
+    Q.layers = p->d_players;
+    Q.n_stages = int(p->stages.size());
+    Q.n_layers = int(p->layers.size());
+    Q.D = p->D;
+    Q.learn = p->learn;
+    Q.act_delay = p->act_delay;
+    Q.G = p->G;
+    Q.F = F;
+    Q.loss = p->loss;
+    Q.lr = p->lr;
+    Q.xs = first ? p->xs_pad : nullptr;
+    Q.ldx = ld0;
+    Q.ys = ys_dev;
+    Q.yhist = p->yhist;
+    Q.yh = p->yh;
+    Q.outs = outs_dev;
+    Q.loss_part = last ? p->loss_part : nullptr;
+    Q.t0 = p->t_next;
+    Q.n = int(n);
+    Q.tick_end = p->d_tick_end;
+    Q.status = p->d_status;
+    Q.bad_target = p->d_bad_target;
+    Q.timeout_ns = p->timeout_ns;
+    Q.nslot = p->pn_nslot;
+    Q.va_off = p->pn_va;
+    Q.vb_off = p->pn_vb;
+    Q.sown_off = p->pn_sown;
+    Q.sah_off = p->pn_sah;
+    Q.red_off = p->pn_red;
+    Q.bar_off = p->pn_bar;
+    Q.desc_off = p->pn_desc;
+    Q.bias_off = p->pn_bias;
+    Q.pf_chunks = p->pn_pf;
+    Q.policy = p->policy;
+    Q.trace = p->d_trace;
+    Q.trace_cap = p->trace_cap;
+    Q.trace_cta = p->trace_cta;
+    Q.jitter = P.jitter;
+    Q.jitter_mask = P.jitter_mask;
+    void* qargs[] = {&Q};
+    CUDA_TRY(cudaEventRecord(p->ev0, p->stream));
+    CUDA_TRY(cudaLaunchCooperativeKernel((const void*)pt::panel_kernel<0>, dim3(p->G), dim3(pt::NTHREADS), qargs,
+                                         size_t(p->pn_smem), p->stream));
+    CUDA_TRY(cudaEventRecord(p->ev1, p->stream));
+  } else if (p->tile) {
     pt::TParams T;
     memset(&T, 0, sizeof(T));
     T.stages = p->d_tstages;
@@ -1102,6 +1382,21 @@ int pt_set_params(pt_pipeline* p, int32_t layer, const float* W, const float* b,
   if (!Lh) return fail(PT_EINVAL, why);
   const cudaMemcpyKind k = where == PT_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
   CUDA_TRY(cudaStreamSynchronize(p->stream));
+  if (p->panel) {
+    // row-major staging -> the tiled buffer the next forward reads; the pending update of
+    // earlier ticks no longer applies to this layer
+    if (W) {
+      const size_t nw = size_t(Lh->n_out) * Lh->n_in;
+      PT_TRY(panel_rowbuf(p, nw));
+      CUDA_TRY(cudaMemcpyAsync(p->rowbuf, W, nw * 4, k, p->stream));
+      pt::pn_to_tiles<<<592, 256, 0, p->stream>>>(p->rowbuf, Lh->Wt[panel_cur(p)], Lh->n_out, Lh->n_in, Lh->R, Lh->C);
+      CUDA_TRY(cudaGetLastError());
+      Lh->set_tick = p->t_next;
+    }
+    if (b) CUDA_TRY(cudaMemcpyAsync(Lh->b, b, size_t(Lh->n_out) * 4, k, p->stream));
+    CUDA_TRY(cudaStreamSynchronize(p->stream));
+    return W ? upload_panel_desc(p) : PT_OK;
+  }
   if (W)
     CUDA_TRY(cudaMemcpy2D(Lh->W, size_t(Lh->ld_in) * 4, W, size_t(Lh->n_in) * 4, size_t(Lh->n_in) * 4,
                           size_t(Lh->n_out), k));
@@ -1119,6 +1414,33 @@ int pt_get_params(pt_pipeline* p, int32_t layer, float* W, float* b, int32_t whe
   if (!Lh) return fail(PT_EINVAL, why);
   const cudaMemcpyKind k = where == PT_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
   CUDA_TRY(cudaStreamSynchronize(p->stream));
+  if (p->panel) {
+    if (W) {
+      // W^(T) = the stored W^(T-1) plus the update of tick T-1, if the next forward would apply it
+      const long long T = p->t_next;
+      const int h = stage_of_layer(p, layer);
+      const bool pend = p->learn && p->lr != 0.f && T - 1 >= 2LL * p->D - h - 1 && T - 1 >= Lh->set_tick;
+      const u64* sdel = nullptr;
+      const u64* ahat = nullptr;
+      if (pend) {
+        const StageHost& S = p->stages[h - 1 - p->local_first];
+        const long long Cp = (h < p->D && p->act_delay) ? T - 2 : T - 1;
+        const size_t li = size_t(layer - p->layer_base);
+        sdel = Lh->dst ? Lh->dst + size_t((T - 1) & 1) * Lh->R * pt::PN_TS
+                       : p->layers[li + 1].gin[0] + size_t((T - 1) & 1) * p->layers[li + 1].C * pt::PN_TS;
+        ahat = S.cache + size_t(Cp & 3) * S.cache_words + Lh->cache_in;
+      }
+      const size_t nw = size_t(Lh->n_out) * Lh->n_in;
+      PT_TRY(panel_rowbuf(p, nw));
+      pt::pn_from_tiles<<<592, 256, 0, p->stream>>>(Lh->Wt[panel_cur(p)], p->rowbuf, Lh->n_out, Lh->n_in, Lh->C, sdel,
+                                                    ahat, p->lr);
+      CUDA_TRY(cudaGetLastError());
+      CUDA_TRY(cudaMemcpyAsync(W, p->rowbuf, nw * 4, k, p->stream));
+    }
+    if (b) CUDA_TRY(cudaMemcpyAsync(b, Lh->b, size_t(Lh->n_out) * 4, k, p->stream));
+    CUDA_TRY(cudaStreamSynchronize(p->stream));
+    return PT_OK;
+  }
   if (W)
     CUDA_TRY(cudaMemcpy2D(W, size_t(Lh->n_in) * 4, Lh->W, size_t(Lh->ld_in) * 4, size_t(Lh->n_in) * 4,
                           size_t(Lh->n_out), k));
@@ -1196,7 +1518,7 @@ int64_t pt_tick(pt_pipeline* p) { return p ? p->t_next : -1; }
 
 int32_t pt_kernel_path(const pt_pipeline* p) {
   if (!p) return fail(PT_EINVAL, "null handle");
-  return p->tile ? PT_PATH_TILE : PT_PATH_TICK;
+  return p->tile ? PT_PATH_TILE : p->panel ? PT_PATH_PANEL : PT_PATH_TICK;
 }
 
 int pt_set_trace(pt_pipeline* p, int32_t cta, int32_t cap) {

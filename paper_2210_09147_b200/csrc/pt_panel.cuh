@@ -1,0 +1,1085 @@
+// pt_panel.cuh: the batch-1 panel kernel for sm_100a (SGD; MSE or softmax-CE).
+//
+// Same tick contract as pt::tick_kernel (reference SPEC.md:217-225,
+// 253-257), with a weight layout and work split that take the backward's
+// cross-CTA reduction off the critical path (profiles/round2_step_bench.md).
+//
+// Weight layout. Layer l is a grid of R x C tiles of 16 x 16 fp32 (1 KB), row-block major:
+// tile (rb, cb) at ((rb * C) + cb) * 256 floats, row-major inside the tile. Padding rows and
+// columns are zero and stay zero. Two buffers per layer (see "deferred update").
+//
+// Work split. CTA k owns row blocks rows_of(R, k, G) in the forward and column blocks
+// rows_of(C, k, G) in the backward:
+//   F_l : z[rows of rb] = W[rb, :] a       reads row block rb (C contiguous tiles, 1-D bulk)
+//   B_l : g[cols of cb] = W[:, cb]^T delta  reads column panel cb (R tiles, 1 KB each, 3-D
+//                                           TMA tensor copies of 32 tiles)
+// Both steps end in an all-gather of a tagged vector (every CTA needs the whole previous
+// vector); no step has a cross-CTA reduction.
+//
+// Deferred update. B_l(t) only READS W^(t) (4 B/weight). The rank-1 update
+// W^(t+1) = W^(t) - lr delta_t a_hat_t^T is applied by F_l(t+1) to each tile as soon as it
+// lands in shared memory, before F's input vector is there ("update-ahead"), and the
+// consumer threads store the result straight to the other buffer (8 B/weight): 12 B/weight
+// per tick, the algorithmic bytes of the fused tick kernel. F_l(t) reads buffer (t-1)&1 and
+// writes buffer t&1; B_l(t) reads buffer (t-1)&1 too and rebuilds W^(t) element by element
+// with the same fmaf F used, so both see bit-identical weights. The pending update of a
+// run's last tick is applied by the next run's F (or by pt_get_params).
+//
+// Backward vectors. The CTA that publishes g_in of layer l+1 for its columns multiplies by
+// act'(a_l) itself, so the published vector IS delta_l (tagged, tick parity). It is the
+// dependency of B_l(t) and, one tick later, the deferred update's delta (F_l(t+1): own rows;
+// B_l(t+1): all rows). A stage's last layer keeps its delta in L.dst (from the loss or from
+// the downstream stage's gradient).
+//
+// Synchronisation (cross-CTA data are tagged words {value, tick+1}, as in the tick kernel):
+//   - tick barrier (learning): a CTA starts tick t once every CTA finished tick t-1. It orders
+//     the weight stores of F(t) (buffer t&1) after every B(t-1) read of that buffer, and it
+//     bounds every ring of per-tick data (cache mod 4, delta mod 2) to one tick of lag;
+//   - the producer issues tick-t backward loads (column panels from every CTA's F(t-1)
+//     stores) once tick t-1 is finished everywhere (same counter), and forward loads of its
+//     own rows once its consumers have fenced the previous tick's stores of that layer;
+//   - stage exchange: the tick kernel's tagged inslot / gslot words and credit counters, so
+//     neighbouring stages may live in another process / on another GPU (IPC, NVLink).
+#pragma once
+#include <cuda.h>
+
+#include "pt_kernels.cuh"
+#include "pt_tc.cuh"
+
+namespace pt {
+
+constexpr int PN_TS = 16;                       // tile side
+constexpr int PN_TILE = PN_TS * PN_TS;          // floats per tile (1 KB)
+constexpr int PN_CT = 32;                       // tiles per chunk (one 32 KB ring slot)
+constexpr int PN_SLOT_FLOATS = PN_CT * PN_TILE;
+constexpr int PN_MAXSLOT = 8;
+
+struct PLayer {
+  float* W[2];               // tiled weights, two buffers
+  const CUtensorMap* tm[2];  // 3-D maps {256 floats, C, R} of W[0] / W[1]: column-panel boxes of 32 tiles
+  float* b;                  // bias [n_out] (the owner CTA keeps its rows in smem during a launch)
+  u64* gin[2];               // tagged delta of the previous layer = act' * g_in, [C*16] per tick parity
+  u64* dst;                  // stage's last layer: tagged delta [2][R*16] per tick parity
+  const u64* dsrc;           // this layer's delta vector [2][R*16]: the next layer's gin or dst
+  int dsrc_stride;           // words between the two parities of dsrc
+  int n_in, n_out, R, C, act;
+  int cache_in, cache_out;   // word offsets of a_{l-1}, a_l in a stage cache slot
+  long long set_tick;        // pt_set_params at this tick discarded the pending update of earlier ticks
+};
+
+struct PStage {
+  int h, first, k;
+  int G_up, G_down, up_remote, down_remote;
+  int ld0, ldk;              // stage slot strides (words)
+  u64* cache[4];             // tagged activation cache slots, tick mod 4
+  u64* inslot[2];
+  u64* gslot[2];
+  u64* peer_inslot[2];
+  u64* peer_gslot[2];
+  u64* act_credit;
+  u64* g_credit;
+  u64* peer_act_credit;
+  u64* peer_g_credit;
+};
+
+struct PParams {
+  const PStage* stages;
+  const PLayer* layers;
+  int n_stages, n_layers, D, learn, act_delay, G, F, loss;
+  float lr;
+  const float* xs;  // padded [n][ldx] (stage 1 local)
+  int ldx;
+  const float* ys;  // [n][Fy] targets of this run
+  const float* yhist;
+  int yh;
+  float* outs;      // [n][F]
+  float* loss_part; // [n][G]
+  long long t0;
+  int n;
+  u64* tick_end;    // cumulative CTA-ticks since create
+  int* status;
+  long long* bad_target;
+  unsigned long long timeout_ns;
+  int nslot, va_off, vb_off, sown_off, sah_off, red_off, bar_off, desc_off, bias_off;
+  int policy;
+  int pf_chunks;    // L2 prefetch distance of the producer (chunks)
+  u64* trace;
+  int trace_cap, trace_cta;
+  int jitter, jitter_mask;
+};
+
+__device__ __forceinline__ int cmod4(long long t) { return int(t & 3); }  // two's complement: -1 -> 3
+
+__device__ __forceinline__ bool pn_upd(const PParams& P, int h, long long t) {
+  return P.learn && P.lr != 0.f && t >= 2LL * P.D - h - 1;  // warm-up gate SPEC.md:254
+}
+// the update of tick t-1 is still to be applied to layer L at tick t
+__device__ __forceinline__ bool pn_pending(const PParams& P, const PLayer& L, int h, long long t) {
+  return pn_upd(P, h, t - 1) && t - 1 >= L.set_tick;
+}
+// the cache tick whose activations B(t) uses (act_delay reading)
+__device__ __forceinline__ long long pn_ct(const PParams& P, int h, long long t) {
+  return (h < P.D && P.act_delay) ? t - 1 : t;
+}
+
+__device__ __forceinline__ bool pn_watchdog(const PParams& P, uint64_t t_start) {
+  if (ld_volatile_s32(P.status) != ST_OK) return true;
+  if (globaltimer() - t_start > P.timeout_ns) {
+    atomicCAS(P.status, ST_OK, ST_TIMEOUT);
+    return true;
+  }
+  return false;
+}
+
+__device__ __noinline__ void pn_wait_cnt(const u64* p, u64 target, const PParams& P) {
+  if (p == nullptr || target == 0) return;
+  if (ld_acquire_sys(p) >= target) return;
+  const uint64_t t_start = globaltimer();
+  for (unsigned it = 1;; ++it) {
+    if (ld_acquire_sys(p) >= target) return;
+    if ((it & 63u) == 0 && pn_watchdog(P, t_start)) return;
+  }
+}
+
+__device__ __forceinline__ u64 pn_ld(const u64* p, bool sys) { return sys ? ld_tv_sys(p) : ld_tv_gpu(p); }
+
+// resolve one tagged word (re-poll until its tag matches)
+__device__ __forceinline__ float pn_resolve(const u64* p, u64 v, uint32_t tag, bool sys, const PParams& P) {
+  if (tv_tag(v) == tag) return tv_val(v);
+  const uint64_t t_start = globaltimer();
+  for (unsigned it = 1;; ++it) {
+    v = pn_ld(p, sys);
+    if (tv_tag(v) == tag) break;
+    if ((it & 31u) == 0 && pn_watchdog(P, t_start)) break;
+  }
+  return tv_val(v);
+}
+
+__device__ __forceinline__ void pn_trace(const PParams& P, int& idx, int limit, int code) {
+  if (P.trace != nullptr && blockIdx.x == P.trace_cta && idx < limit)
+    P.trace[idx++] = (u64(code) << 56) | (globaltimer() & 0x00FFFFFFFFFFFFFFull);
+}
+// race detector: random stalls at the step phases (compiled into libpartime_b200_jitter.so only)
+__device__ __forceinline__ void pn_jitter(const PParams& P, int code) {
+#ifdef PT_JITTER_BUILD
+  if (P.jitter <= 0) return;
+  uint32_t x = uint32_t(globaltimer()) ^ (blockIdx.x * 0x9E3779B9u) ^ ((threadIdx.x >> 5) * 0x85EBCA6Bu) ^
+               (uint32_t(code) * 0xC2B2AE35u);
+  x ^= x >> 16;
+  x *= 0x7FEB352Du;
+  x ^= x >> 15;
+  if ((x & uint32_t(P.jitter_mask)) == 0) {
+    const uint64_t t0 = globaltimer(), d = (x >> 8) % uint32_t(P.jitter);
+    while (globaltimer() - t0 < d) __nanosleep(1000);
+  }
+#else
+  (void)P;
+  (void)code;
+#endif
+}
+
+// tagged words [n] at p into dst[0..n) (scaled) by the consumer threads; the first NCT loads
+// were issued earlier (v0 = the value this thread loaded from p[tid], when tid < n)
+__device__ __forceinline__ void pn_small(const u64* p, int n, u64 v0, uint32_t tag, float scale, float* dst,
+                                         const PParams& P) {
+  for (int j = threadIdx.x; j < n; j += NCT) {
+    const u64 v = j < NCT ? v0 : ld_tv_gpu(p + j);
+    dst[j] = scale * pn_resolve(p + j, v, tag, false, P);
+  }
+}
+
+struct PV {
+  const u64* p;  // null: not gathered (values read as 0)
+  uint32_t tag;
+  int sys;
+};
+
+// Pairs of words a consumer thread gathers per batch: j = base + 2 tid + 2 NCT q, q < 4.
+// issue() puts the loads in flight; stale() re-polls every stale pair together, so a round
+// costs one L2 round trip however many words were late.
+struct PBatch {
+  u64 w[8];
+  __device__ __forceinline__ void issue(const PV& v, int n, int base) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int j = base + 2 * int(threadIdx.x) + 2 * NCT * q;
+      if (j < n && v.p) {
+        if (v.sys) ld2_tv_sys(v.p + j, w[2 * q], w[2 * q + 1]);
+        else ld2_tv_gpu(v.p + j, w[2 * q], w[2 * q + 1]);
+      } else {
+        w[2 * q] = w[2 * q + 1] = pack_tv(0.f, v.tag);
+      }
+    }
+  }
+  __device__ __forceinline__ bool stale(const PV& v, int base) {
+    bool st = false;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int j = base + 2 * int(threadIdx.x) + 2 * NCT * q;
+      if (tv_tag(w[2 * q]) != v.tag || tv_tag(w[2 * q + 1]) != v.tag) {
+        st = true;
+        if (v.sys) ld2_tv_sys(v.p + j, w[2 * q], w[2 * q + 1]);
+        else ld2_tv_gpu(v.p + j, w[2 * q], w[2 * q + 1]);
+      }
+    }
+    return st;
+  }
+  __device__ __forceinline__ void settle(const PV& v, int base, const PParams& P) {
+    uint64_t t_start = 0;
+    for (unsigned it = 0; stale(v, base); ++it) {
+      if (it == 0) t_start = globaltimer();
+      if ((it & 15u) == 15u && pn_watchdog(P, t_start)) break;
+    }
+  }
+};
+
+// All-gather of up to NV tagged vectors [n] (n even); put(j, x) receives words j, j+1 of each
+template <int NV, class Put>
+__device__ __forceinline__ void pn_gather(const PV (&v)[NV], int n, const PParams& P, Put&& put) {
+  for (int base = 0; base < n; base += 4 * 2 * NCT) {
+    PBatch b[NV];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) b[k].issue(v[k], n, base);
+    uint64_t t_start = 0;
+    for (unsigned it = 0;; ++it) {
+      bool st = false;
+#pragma unroll
+      for (int k = 0; k < NV; ++k) st |= b[k].stale(v[k], base);
+      if (!st) break;
+      if (it == 0) t_start = globaltimer();
+      if ((it & 15u) == 15u && pn_watchdog(P, t_start)) break;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int j = base + 2 * int(threadIdx.x) + 2 * NCT * q;
+      if (j < n) {
+        float x[NV][2];
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+          x[k][0] = tv_val(b[k].w[2 * q]);
+          x[k][1] = tv_val(b[k].w[2 * q + 1]);
+        }
+        put(j, x);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// producer: every chunk of every step in the consumers' order, plus an L2 prefetch cursor
+// pf_chunks ahead
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void pn_tma_load_3d(void* dst, const CUtensorMap* tm, int c0, int c1, int c2,
+                                               uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, "
+      "%3, %4}], [%5], %6;" ::"r"(smem_u32(dst)),
+      "l"(tm), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void pn_tma_prefetch_3d(const CUtensorMap* tm, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(tm), "r"(c0), "r"(c1),
+               "r"(c2)
+               : "memory");
+}
+
+// Schedule cursor: this CTA's chunks in the consumers' exact order (ticks x local stages x
+// [F_0..F_{k-1}, B_{k-1}..B_0] x own blocks x chunks); backward steps without weight reads
+// (stage 1, layer 0) have no chunks. fstep counts forward steps from the launch start.
+struct PCursor {
+  int ti, s, st, blk, off;  // tick, stage, step, own block, chunk offset (tiles) in the block
+  int b0, b1, len, nsteps, k, fstep;
+  bool done;
+  const PLayer* L;
+  __device__ __forceinline__ bool fwd() const { return st < k; }
+  __device__ void begin_step(const PParams& P, const PStage* stages, const PLayer* layers) {
+    const PStage& S = stages[s];
+    k = S.k;
+    nsteps = P.learn ? 2 * S.k : S.k;
+    const int i = st < S.k ? st : 2 * S.k - 1 - st;
+    L = &layers[S.first + i];
+    Rows R;
+    if (st < S.k) {
+      R = rows_of(L->R, blockIdx.x, P.G);
+      len = L->C;
+    } else {
+      R = (S.h == 1 && i == 0) ? Rows{0, 0} : rows_of(L->C, blockIdx.x, P.G);
+      len = L->R;
+    }
+    b0 = R.r0;
+    b1 = R.r1;
+    blk = b0;
+    off = 0;
+  }
+  __device__ void next_step(const PParams& P, const PStage* stages, const PLayer* layers) {
+    if (st < k) ++fstep;
+    if (++st == nsteps) {
+      st = 0;
+      if (++s == P.n_stages) {
+        s = 0;
+        if (++ti == P.n) {
+          done = true;
+          return;
+        }
+      }
+    }
+    begin_step(P, stages, layers);
+  }
+  __device__ void settle(const PParams& P, const PStage* stages, const PLayer* layers) {
+    while (!done && blk >= b1) next_step(P, stages, layers);
+  }
+  __device__ void init(const PParams& P, const PStage* stages, const PLayer* layers) {
+    ti = s = st = fstep = 0;
+    done = P.n <= 0;
+    if (done) return;
+    begin_step(P, stages, layers);
+    settle(P, stages, layers);
+  }
+  __device__ void advance(const PParams& P, const PStage* stages, const PLayer* layers) {
+    off += PN_CT;
+    if (off >= len) {
+      off = 0;
+      ++blk;
+      settle(P, stages, layers);
+    }
+  }
+  __device__ __forceinline__ long long t(const PParams& P) const { return P.t0 + ti; }
+  __device__ __forceinline__ int ntiles() const { return min(PN_CT, len - off); }
+  __device__ __forceinline__ size_t foff() const { return (size_t(blk) * L->C + off) * PN_TILE; }
+};
+
+// fwd_fenced: forward steps whose consumer weight stores are fenced for the async proxy
+// (count from the launch start, written by consumer thread 0)
+__device__ void pn_producer(const PParams& P, const PLayer* layers, const PStage* stages, float* ring,
+                            uint64_t* full, uint64_t* empty, const int* fwd_fenced, int nF) {
+  const uint64_t pol = P.policy == 1 ? policy_evict_normal() : policy_evict_first();
+  const int G = P.G, nslot = P.nslot;
+  uint32_t chunk = 0;
+  bool dead = false;
+  int tr = P.trace_cap / 2;
+  PCursor cur, pf;
+  cur.init(P, stages, layers);
+  pf.init(P, stages, layers);
+  uint32_t pf_idx = 0;
+  auto top_up = [&]() {
+    while (!pf.done && pf_idx < chunk + uint32_t(P.pf_chunks)) {
+      const long long t = pf.t(P);
+      if (pf.fwd()) {
+        prefetch_l2(pf.L->W[P.learn ? int((t - 1) & 1) : 0] + pf.foff(), uint32_t(pf.ntiles()) * PN_TILE * 4u);
+      } else {
+        pn_tma_prefetch_3d(pf.L->tm[int((t - 1) & 1)], 0, pf.blk, pf.off);
+      }
+      pf.advance(P, stages, layers);
+      ++pf_idx;
+    }
+  };
+  top_up();
+  int raw_ti = 0;  // backward loads of ticks <= raw_ti may start (every CTA finished tick ti-1)
+  while (!cur.done && !dead) {
+    const int ti = cur.ti;
+    const long long t = cur.t(P);
+    if (P.learn && ti > 0) {
+      if (cur.fwd()) {
+        // my rows of this layer were stored by my consumers at tick ti-1: fenced yet?
+        const int need = cur.fstep - nF + 1;
+        if (ld_acquire_cta_s32(fwd_fenced) < need) {
+          const uint64_t t0 = globaltimer();
+          while (ld_acquire_cta_s32(fwd_fenced) < need) {
+            top_up();
+            if (pn_watchdog(P, t0)) {
+              dead = true;
+              break;
+            }
+          }
+        }
+      } else if (ti > raw_ti) {
+        // column panels hold every CTA's tick ti-1 stores
+        pn_wait_cnt(P.tick_end, u64(G) * u64(t), P);
+        fence_proxy_async_global();
+        raw_ti = ti;
+      }
+    }
+    const int slot = int(chunk % uint32_t(nslot));
+    const uint32_t use = chunk / uint32_t(nslot);
+    if (use > 0) {
+      const uint64_t t0 = globaltimer();
+      while (!dead && !mbar_try_wait(&empty[slot], (use - 1) & 1u)) {
+        top_up();
+        if (pn_watchdog(P, t0)) dead = true;
+      }
+    }
+    if (dead) break;
+    float* sdst = ring + size_t(slot) * PN_SLOT_FLOATS;
+    if (cur.fwd()) {
+      pn_trace(P, tr, P.trace_cap - P.trace_cap / 4, 40);
+      pn_jitter(P, 40);
+      const uint32_t bytes = uint32_t(cur.ntiles()) * PN_TILE * 4u;
+      mbar_arrive_expect_tx(&full[slot], bytes);
+      bulk_g2s(sdst, cur.L->W[P.learn ? int((t - 1) & 1) : 0] + cur.foff(), bytes, &full[slot], pol);
+    } else {
+      pn_trace(P, tr, P.trace_cap - P.trace_cap / 4, 41);
+      pn_jitter(P, 41);
+      mbar_arrive_expect_tx(&full[slot], uint32_t(PN_SLOT_FLOATS) * 4u);
+      pn_tma_load_3d(sdst, cur.L->tm[int((t - 1) & 1)], 0, cur.blk, cur.off, &full[slot], pol);
+    }
+    ++chunk;
+    cur.advance(P, stages, layers);
+    top_up();
+  }
+  if (dead) {
+    const uint64_t t0 = globaltimer();
+    while (globaltimer() - t0 < 2000000ull) {
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// consumers
+// ---------------------------------------------------------------------------
+struct PSmem {
+  float* ring;
+  float* va;    // F: input a          B: delta
+  float* vb;    // F: a_hat (pending)  B: -lr * delta_{t-1} (pending)
+  float* sown;  // F: -lr * delta_{t-1} of own rows
+  float* sah;   // B: a_hat_{t-1} of own columns
+  float* red;   // 2 x 128 floats
+  float* scal;  // 64 floats
+  float* bias;  // own forward rows of every local layer's bias, resident for the launch
+  int* boff;    // per layer: offset of its rows in `bias`
+  int* flags;   // [0] forward steps fenced (producer's RAW wait)
+  uint64_t* full;
+  uint64_t* empty;
+};
+
+__device__ __forceinline__ void pn_fma4(float4& w, float s, float4 a) {
+  w.x = fmaf(s, a.x, w.x);
+  w.y = fmaf(s, a.y, w.y);
+  w.z = fmaf(s, a.z, w.z);
+  w.w = fmaf(s, a.w, w.w);
+}
+
+// Forward chunk, update half: W^(t) = W^(t-1) + sc * a_hat (pending) on this thread's 8 tile
+// rows, written back into the slot (for the dot) and to the next buffer (HBM). All loads of a
+// batch are issued before any store.
+template <bool PEND, bool FULL>
+__device__ __forceinline__ void pn_fupdate(float* wb, float* gdst, const float* vb, float sc, int nt, int tg) {
+#pragma unroll
+  for (int hb = 0; hb < 2; ++hb) {
+    float4 w[4], ah[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int tt = (hb * 4 + q) * 4 + tg;
+      const bool ok = FULL || tt < nt;
+      w[q] = ok ? lds4(wb + tt * PN_TILE) : make_float4(0.f, 0.f, 0.f, 0.f);
+      if (PEND) ah[q] = ok ? lds4(vb + tt * PN_TS) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int tt = (hb * 4 + q) * 4 + tg;
+      if (PEND) pn_fma4(w[q], sc, ah[q]);
+      if (FULL || tt < nt) {
+        if (PEND) *reinterpret_cast<float4*>(wb + tt * PN_TILE) = w[q];
+        __stcs(reinterpret_cast<float4*>(gdst + tt * PN_TILE), w[q]);
+      }
+    }
+  }
+}
+
+// Forward chunk, dot half: this thread's partial of row tr over its 8 tiles (two accumulators,
+// fixed combination order)
+template <bool FULL>
+__device__ __forceinline__ float pn_fdot(const float* wb, const float* va, int nt, int tg) {
+  float4 w[8], a[8];
+#pragma unroll
+  for (int p = 0; p < 8; ++p) {
+    const int tt = p * 4 + tg;
+    const bool ok = FULL || tt < nt;
+    w[p] = ok ? lds4(wb + tt * PN_TILE) : make_float4(0.f, 0.f, 0.f, 0.f);
+    a[p] = ok ? lds4(va + tt * PN_TS) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  float z0 = 0.f, z1 = 0.f;
+#pragma unroll
+  for (int p = 0; p < 8; p += 2) {
+    z0 += dot4(w[p], a[p]);
+    z1 += dot4(w[p + 1], a[p + 1]);
+  }
+  return z0 + z1;
+}
+
+// Backward chunk: acc += W^(t)[rows][own 4 columns] * delta[rows], W^(t) rebuilt from the
+// stored W^(t-1) with the pending update (the same fmaf as the forward).
+template <bool PEND, bool FULL>
+__device__ __forceinline__ void pn_bchunk(const float* wb, const float* dl, const float* sp, float4 ah4, int nt,
+                                          int tg, float4& acc) {
+  float4 w[8];
+  float d[8], s[8];
+#pragma unroll
+  for (int p = 0; p < 8; ++p) {
+    const int tt = p * 4 + tg;
+    const bool ok = FULL || tt < nt;
+    w[p] = ok ? lds4(wb + tt * PN_TILE) : make_float4(0.f, 0.f, 0.f, 0.f);
+    d[p] = ok ? dl[tt * PN_TS] : 0.f;
+    if (PEND) s[p] = ok ? sp[tt * PN_TS] : 0.f;
+  }
+#pragma unroll
+  for (int p = 0; p < 8; ++p) {
+    if (PEND) pn_fma4(w[p], s[p], ah4);
+    acc.x = fmaf(w[p].x, d[p], acc.x);
+    acc.y = fmaf(w[p].y, d[p], acc.y);
+    acc.z = fmaf(w[p].z, d[p], acc.z);
+    acc.w = fmaf(w[p].w, d[p], acc.w);
+  }
+}
+
+// deterministic CTA-wide max / sum over the consumer threads (result on every thread)
+__device__ __forceinline__ float pn_cta_red(float v, bool is_max, const PSmem& sm) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float u = __shfl_xor_sync(0xffffffffu, v, o);
+    v = is_max ? fmaxf(v, u) : v + u;
+  }
+  cons_sync(NCT);
+  if (lane == 0) sm.scal[warp] = v;
+  cons_sync(NCT);
+  float r = sm.scal[0];
+  for (int w = 1; w < NCW; ++w) r = is_max ? fmaxf(r, sm.scal[w]) : r + sm.scal[w];
+  cons_sync(NCT);
+  return r;
+}
+
+// target row of sample sid (stage D): the run's ys or the target history ring
+__device__ __forceinline__ const float* pn_target(const PParams& P, long long sid, int Fy) {
+  if (sid < 0) return nullptr;
+  if (sid >= P.t0) return P.ys ? P.ys + size_t(sid - P.t0) * Fy : nullptr;
+  return P.yhist ? P.yhist + size_t(sid % P.yh) * Fy : nullptr;
+}
+
+// wait for one ring slot's data (consumer threads); the slot / phase cursor advances
+__device__ __forceinline__ int pn_take(const PSmem& sm, int& cslot, uint32_t& cphase, const PParams& P) {
+  const int slot = cslot;
+  const uint32_t ph = cphase;
+  if (++cslot == P.nslot) {
+    cslot = 0;
+    cphase ^= 1u;
+  }
+  if (!mbar_try_wait(&sm.full[slot], ph)) {
+    const uint64_t t0 = globaltimer();
+    while (!mbar_try_wait(&sm.full[slot], ph))
+      if (pn_watchdog(P, t0)) break;
+  }
+  return slot;
+}
+
+template <int DUMMY>
+__global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constant__ PParams P) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  PSmem sm;
+  sm.ring = reinterpret_cast<float*>(smem_raw);
+  sm.va = reinterpret_cast<float*>(smem_raw + P.va_off);
+  sm.vb = reinterpret_cast<float*>(smem_raw + P.vb_off);
+  sm.sown = reinterpret_cast<float*>(smem_raw + P.sown_off);
+  sm.sah = reinterpret_cast<float*>(smem_raw + P.sah_off);
+  sm.red = reinterpret_cast<float*>(smem_raw + P.red_off);
+  sm.scal = sm.red + 256;
+  sm.flags = reinterpret_cast<int*>(sm.scal + 64);
+  sm.full = reinterpret_cast<uint64_t*>(smem_raw + P.bar_off);
+  sm.empty = sm.full + P.nslot;
+  PLayer* s_layers = reinterpret_cast<PLayer*>(smem_raw + P.desc_off);
+  PStage* s_stages = reinterpret_cast<PStage*>(s_layers + P.n_layers);
+  sm.boff = reinterpret_cast<int*>(s_stages + P.n_stages);
+  sm.bias = reinterpret_cast<float*>(smem_raw + P.bias_off);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int c = blockIdx.x, G = P.G;
+  if (tid == 0) {
+    for (int s = 0; s < P.nslot; ++s) {
+      mbar_init(&sm.full[s], 1);
+      mbar_init(&sm.empty[s], NCW);
+    }
+    sm.flags[0] = 0;
+    fence_mbar_init();
+  }
+  {
+    const int* src = reinterpret_cast<const int*>(P.layers);
+    int* dst = reinterpret_cast<int*>(s_layers);
+    for (int j = tid; j < P.n_layers * int(sizeof(PLayer) / 4); j += NTHREADS) dst[j] = src[j];
+    src = reinterpret_cast<const int*>(P.stages);
+    dst = reinterpret_cast<int*>(s_stages);
+    for (int j = tid; j < P.n_stages * int(sizeof(PStage) / 4); j += NTHREADS) dst[j] = src[j];
+  }
+  __syncthreads();
+  int nF = 0;  // forward steps per tick
+  for (int s = 0; s < P.n_stages; ++s) nF += s_stages[s].k;
+  if (tid == 0) {
+    int off = 0;
+    for (int l = 0; l < P.n_layers; ++l) {
+      sm.boff[l] = off;
+      const Rows RB = rows_of(s_layers[l].R, c, G);
+      off += (RB.r1 - RB.r0) * PN_TS;
+    }
+  }
+  __syncthreads();
+  for (int l = 0; l < P.n_layers; ++l) {
+    const PLayer& L = s_layers[l];
+    const Rows RB = rows_of(L.R, c, G);
+    for (int j = tid; j < (RB.r1 - RB.r0) * PN_TS; j += NTHREADS) {
+      const int row = RB.r0 * PN_TS + j;
+      sm.bias[sm.boff[l] + j] = row < L.n_out ? L.b[row] : 0.f;
+    }
+  }
+  __syncthreads();
+  if (warp == NCW) {
+    if (lane == 0) {
+      // maps written by the host: acquire them for the async proxy (a new handle may reuse a
+      // freed handle's map address; see pt_tc.cuh)
+      for (int l = 0; l < P.n_layers && P.learn; ++l)
+        for (int b = 0; b < 2; ++b) {
+          tma_fence_desc_acquire(s_layers[l].tm[b]);
+          tma_prefetch_desc(s_layers[l].tm[b]);
+        }
+      pn_producer(P, s_layers, s_stages, sm.ring, sm.full, sm.empty, sm.flags, nF);
+    }
+    return;
+  }
+  // thread's place in a chunk: float4 f4 of row tr of tiles tg, tg+4, ... (8 tiles of 32)
+  const int f4 = tid & 3, tr = (tid >> 2) & 15, tg = tid >> 6;
+  const int toff = tr * PN_TS + f4 * 4;  // this thread's float4 inside a tile
+  int cslot = 0;        // ring slot of the next chunk
+  uint32_t cphase = 0;  // its full-barrier phase parity
+  int fdone = 0;        // forward steps of this launch completed (their stores precede the next fence)
+  int tri = 0;
+  int trc = P.trace_cap - P.trace_cap / 4;  // chunk-ready events: last quarter of the trace buffer
+  const int trl = P.trace_cap / 2;
+  int ev_all = 0;
+#define PN_TR(code)                                                                                \
+  pn_jitter(P, (code));                                                                            \
+  if (tid == 0 && P.trace != nullptr) {                                                            \
+    if (c == P.trace_cta && tri < trl)                                                             \
+      P.trace[tri++] = (u64(code) << 56) | (globaltimer() & 0x00FFFFFFFFFFFFFFull);                \
+    if (P.trace_cta < 0 && ((code) == 4 || (code) == 14)) {                                        \
+      if ((ev_all + 1) * G <= P.trace_cap) P.trace[ev_all * G + c] = globaltimer();               \
+      ++ev_all;                                                                                    \
+    }                                                                                              \
+  }
+#define PN_TRC(code)                                                                               \
+  if (tid == 0 && P.trace != nullptr && c == P.trace_cta && trc < P.trace_cap)                     \
+    P.trace[trc++] = (u64(code) << 56) | (globaltimer() & 0x00FFFFFFFFFFFFFFull);
+  for (int ti = 0; ti < P.n; ++ti) {
+    const long long t = P.t0 + ti;
+    const uint32_t tag_t = tag_of_tick(t);
+    // tick barrier. Learning: every CTA finished tick t-1 (orders this tick's weight stores
+    // after every read of their buffer, and keeps per-tick rings one tick deep). Inference:
+    // lagged by one tick (cache slots only).
+    if (tid == 0) {
+      if (P.learn && t >= 1) pn_wait_cnt(P.tick_end, u64(G) * u64(t), P);
+      else if (!P.learn && t >= 2) pn_wait_cnt(P.tick_end, u64(G) * u64(t - 1), P);
+    }
+    for (int s = 0; s < P.n_stages; ++s) {
+      const PStage& S = s_stages[s];
+      const int h = S.h;
+      u64* Ccur = S.cache[cmod4(t)];
+      // ------------------------------------------------------------------ forward
+      for (int i = 0; i < S.k; ++i) {
+        const PLayer& L = s_layers[S.first + i];
+        const int nin = L.C * PN_TS;
+        const Rows RB = rows_of(L.R, c, G);
+        const int nown = (RB.r1 - RB.r0) * PN_TS;
+        const int nch = (L.C + PN_CT - 1) / PN_CT;  // chunks per row block
+        const bool last = i == S.k - 1;
+        const bool pend = pn_pending(P, L, h, t);
+        const long long Cp = pn_ct(P, h, t - 1);
+        PN_TR(1);
+        // every weight store of earlier forward steps is fenced for the producer's loads
+        if (P.learn) fence_proxy_async_global();
+        // the input vector (the dependency): loads in flight now, resolved after the update
+        PV vin{nullptr, 0u, 0};
+        if (i == 0 && h > 1) vin = PV{S.inslot[(t - 1) & 1], tag_of_tick(t - 1), S.up_remote};
+        else if (i > 0) vin = PV{Ccur + L.cache_in, tag_t, 0};
+        PBatch dep;
+        dep.issue(vin, nin, 0);
+        if (pend) {
+          const u64* sop = L.dsrc + size_t((t - 1) & 1) * L.dsrc_stride + RB.r0 * PN_TS;
+          const u64 so = tid < nown ? ld_tv_gpu(sop + tid) : 0ull;
+          PV va1[1] = {PV{S.cache[cmod4(Cp)] + L.cache_in, tag_of_tick(Cp), 0}};
+          pn_gather<1>(va1, nin, P, [&](int j, const float (&x)[1][2]) {
+            sm.vb[j] = x[0][0];
+            sm.vb[j + 1] = x[0][1];
+          });
+          pn_small(sop, nown, so, tag_of_tick(t - 1), -P.lr, sm.sown, P);
+        }
+        cons_sync(NCT);
+        if (P.learn && tid == 0) st_release_cta_s32(&sm.flags[0], fdone);
+        PN_TR(2);
+        // update-ahead: the pending update of the chunks the ring can hold, before the input
+        // is there; W^(t) goes to the slot and to buffer t&1
+        const int nck = nch * (RB.r1 - RB.r0);
+        const int ua = P.learn ? min(nck, P.nslot) : 0;
+        float* Wn = L.W[int(t & 1)];
+        {
+          int k = 0;
+          int us = cslot;
+          uint32_t up = cphase;
+          for (int rb = RB.r0; rb < RB.r1 && k < ua; ++rb) {
+            const float sc = pend ? sm.sown[(rb - RB.r0) * PN_TS + tr] : 0.f;
+            for (int c0 = 0; c0 < L.C && k < ua; c0 += PN_CT, ++k) {
+              const int nt = min(PN_CT, L.C - c0);
+              const int slot = pn_take(sm, us, up, P);
+              PN_TRC(7);
+              float* wb = sm.ring + size_t(slot) * PN_SLOT_FLOATS + toff;
+              float* gd = Wn + (size_t(rb) * L.C + c0) * PN_TILE + toff;
+              const float* vb = sm.vb + c0 * PN_TS + f4 * 4;
+              if (pend) {
+                if (nt == PN_CT) pn_fupdate<true, true>(wb, gd, vb, sc, nt, tg);
+                else pn_fupdate<true, false>(wb, gd, vb, sc, nt, tg);
+              } else {
+                if (nt == PN_CT) pn_fupdate<false, true>(wb, gd, vb, sc, nt, tg);
+                else pn_fupdate<false, false>(wb, gd, vb, sc, nt, tg);
+              }
+            }
+          }
+        }
+        // the input
+        if (i == 0 && h == 1) {
+          const float* x = P.xs + size_t(ti) * P.ldx;
+          for (int j = tid * 4; j < nin; j += NCT * 4)
+            *reinterpret_cast<float4*>(sm.va + j) = ldcg4(reinterpret_cast<const float4*>(x + j));
+        } else {
+          dep.settle(vin, 0, P);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int j = 2 * tid + 2 * NCT * q;
+            if (j < nin) {
+              sm.va[j] = tv_val(dep.w[2 * q]);
+              sm.va[j + 1] = tv_val(dep.w[2 * q + 1]);
+            }
+          }
+          if (nin > 4 * 2 * NCT) {  // beyond the first batch
+            PV rest[1] = {vin};
+            pn_gather<1>(rest, nin, P, [&](int j, const float (&x)[1][2]) {
+              if (j >= 4 * 2 * NCT) {
+                sm.va[j] = x[0][0];
+                sm.va[j + 1] = x[0][1];
+              }
+            });
+          }
+        }
+        cons_sync(NCT);
+        if (i == 0) {
+          // private copy of the stage input in the cache (inslot is rewritten at t+1)
+          const Rows Q = rows_of(nin, c, G);
+          for (int j = Q.r0 + tid; j < Q.r1; j += NCT) st_tv_gpu(Ccur + L.cache_in + j, pack_tv(sm.va[j], tag_t));
+          if (h > 1 && tid == 0) red_relaxed_sys(S.peer_act_credit, 1);  // inslot read (all threads: cons_sync above)
+        }
+        PN_TR(3);
+        const bool net_last = last && h == P.D;
+        const long long sid = t - (P.D - 1);
+        const float* y = net_last ? pn_target(P, sid, P.loss == 1 ? 1 : P.F) : nullptr;
+        float lsum = 0.f;
+        int k = 0;
+        for (int rb = RB.r0; rb < RB.r1; ++rb) {
+          const float sc = pend ? sm.sown[(rb - RB.r0) * PN_TS + tr] : 0.f;
+          float z = 0.f;
+          for (int c0 = 0; c0 < L.C; c0 += PN_CT, ++k) {
+            const int nt = min(PN_CT, L.C - c0);
+            const int slot = pn_take(sm, cslot, cphase, P);
+            if (k >= ua) PN_TRC(7);
+            float* wb = sm.ring + size_t(slot) * PN_SLOT_FLOATS + toff;
+            const float* va = sm.va + c0 * PN_TS + f4 * 4;
+            if (k >= ua && P.learn) {
+              // beyond the update-ahead window: update (and store) here
+              float* gd = Wn + (size_t(rb) * L.C + c0) * PN_TILE + toff;
+              const float* vb = sm.vb + c0 * PN_TS + f4 * 4;
+              if (pend) pn_fupdate<true, false>(wb, gd, vb, sc, nt, tg);
+              else pn_fupdate<false, false>(wb, gd, vb, sc, nt, tg);
+            }
+            z += nt == PN_CT ? pn_fdot<true>(wb, va, nt, tg) : pn_fdot<false>(wb, va, nt, tg);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sm.empty[slot]);
+          }
+          z += __shfl_xor_sync(0xffffffffu, z, 1);
+          z += __shfl_xor_sync(0xffffffffu, z, 2);
+          float* rd = sm.red + ((rb - RB.r0) & 1) * 128;
+          if (f4 == 0) rd[tg * PN_TS + tr] = z;
+          cons_sync(NCT);
+          if (tid < PN_TS) {
+            const int row = rb * PN_TS + tid;
+            float a = 0.f;
+            if (row < L.n_out) {
+              const float zz = ((rd[tid] + rd[PN_TS + tid]) + rd[2 * PN_TS + tid]) + rd[3 * PN_TS + tid] +
+                               sm.bias[sm.boff[S.first + i] + (rb - RB.r0) * PN_TS + tid];
+              a = act_fn(L.act, zz);
+            }
+            const u64 w = pack_tv(a, tag_t);
+            st_tv_gpu(Ccur + L.cache_out + row, w);
+            if (last && h < P.D) {
+              if (rb == RB.r0) {
+                if (tid == 0) pn_wait_cnt(S.act_credit, u64(S.G_down) * u64(t), P);  // downstream read slot t&1 at t-1
+                __syncwarp(0xffffu);
+              }
+              if (S.down_remote) st_tv_sys(S.peer_inslot[t & 1] + row, w);
+              else st_tv_gpu(S.peer_inslot[t & 1] + row, w);
+            }
+            if (net_last && row < P.F) {
+              P.outs[size_t(ti) * P.F + row] = a;
+              if (P.loss == 0 && y) {
+                const float d = a - y[row];
+                lsum = fmaf(d, d, lsum);
+              }
+            }
+          }
+        }
+        ++fdone;
+        if (RB.r0 == RB.r1) cons_sync(NCT);  // no chunk loop: every read of va (input copy) is done
+        if (net_last && warp == 0) {
+          // MSE: this CTA's partial of sum (a - y)^2 (the epilogue divides by M*F); softmax-CE:
+          // CTA 0 writes the loss after the full output is gathered (backward, or below)
+          lsum = warp_sum(lsum);
+          if (lane == 0) P.loss_part[size_t(ti) * G + c] = lsum;
+        }
+        PN_TR(4);
+        if (net_last && P.loss == 1 && !P.learn && c == 0 && y) {
+          // inference wave with softmax-CE: CTA 0 gathers the output for the loss
+          PV vo[1] = {PV{Ccur + L.cache_out, tag_t, 0}};
+          pn_gather<1>(vo, L.C * PN_TS, P, [&](int j, const float (&x)[1][2]) {
+            sm.va[j] = x[0][0];
+            sm.va[j + 1] = x[0][1];
+          });
+          cons_sync(NCT);
+          float mx = -INFINITY;
+          for (int f = tid; f < P.F; f += NCT) mx = fmaxf(mx, sm.va[f]);
+          mx = pn_cta_red(mx, true, sm);
+          float se = 0.f;
+          for (int f = tid; f < P.F; f += NCT) se += expf(sm.va[f] - mx);
+          se = pn_cta_red(se, false, sm);
+          if (tid == 0) {
+            const int tgt = int(y[0]);
+            if (!(y[0] >= 0.f && y[0] < float(P.F) && float(tgt) == y[0])) {
+              atomicMin(P.bad_target, sid);
+              P.loss_part[size_t(ti) * G] = 0.f;
+            } else {
+              P.loss_part[size_t(ti) * G] = mx + logf(se) - sm.va[tgt];
+            }
+          }
+        }
+      }
+      if (!P.learn) continue;
+      // ----------------------------------------------------------------- backward
+      const bool upd_now = pn_upd(P, h, t);
+      const long long Ct = pn_ct(P, h, t);
+      u64* Cc = S.cache[cmod4(Ct)];
+      for (int i = S.k - 1; i >= 0; --i) {
+        const PLayer& L = s_layers[S.first + i];
+        const int nout = L.R * PN_TS;
+        const Rows RB = rows_of(L.R, c, G);
+        const Rows CB = rows_of(L.C, c, G);
+        const int ncol = (CB.r1 - CB.r0) * PN_TS;
+        const bool need_gin = !(h == 1 && i == 0);
+        const bool pend = pn_pending(P, L, h, t);
+        const long long Cp = pn_ct(P, h, t - 1);
+        const bool stage_last = i == S.k - 1;
+        const bool loss_src = stage_last && h == P.D;
+        PN_TR(11);
+        // own columns' a_hat_{t-1}: issued now, resolved after the gather
+        u64 ah = 0;
+        const u64* ahp = nullptr;
+        if (pend && need_gin) {
+          ahp = S.cache[cmod4(Cp)] + L.cache_in + CB.r0 * PN_TS;
+          if (tid < ncol) ah = ld_tv_gpu(ahp + tid);
+        }
+        // delta_l(t): the next layer's published vector, or (stage's last layer) the loss
+        // gradient / the downstream stage's g_in times act'; delta_l(t-1) for the rebuild
+        PV vg[3];
+        vg[0] = PV{nullptr, 0u, 0};
+        vg[1] = PV{nullptr, 0u, 0};
+        if (loss_src) {
+          vg[0] = PV{Cc + L.cache_out, tag_t, 0};  // the output a_L(t) (Ct = t at stage D)
+        } else if (stage_last) {
+          vg[0] = PV{S.gslot[(t - 1) & 1], tag_of_tick(t - 1), S.down_remote};
+          vg[1] = PV{Cc + L.cache_out, tag_of_tick(Ct), 0};
+        } else {
+          vg[0] = PV{L.dsrc + size_t(t & 1) * L.dsrc_stride, tag_t, 0};
+        }
+        vg[2] = (pend && need_gin) ? PV{L.dsrc + size_t((t - 1) & 1) * L.dsrc_stride, tag_of_tick(t - 1), 0}
+                                   : PV{nullptr, 0u, 0};
+        const long long sid = t - (P.D - 1);
+        const float* y = loss_src ? pn_target(P, sid, P.loss == 1 ? 1 : P.F) : nullptr;
+        const float g_scale = 2.f / float(P.F);  // d mse / d a (M = 1)
+        const float nlr = -P.lr;
+        pn_gather<3>(vg, nout, P, [&](int j, const float (&x)[3][2]) {
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            float d;
+            if (loss_src) {
+              const float a = x[0][e];
+              if (P.loss == 1) d = a;  // raw output: softmax below
+              else d = (y && j + e < P.F) ? g_scale * (a - y[j + e]) * dact_fn(L.act, a) : 0.f;
+            } else if (stage_last) {
+              d = x[0][e] * dact_fn(L.act, x[1][e]);
+            } else {
+              d = x[0][e];
+            }
+            sm.va[j + e] = d;
+            sm.vb[j + e] = nlr * x[2][e];
+          }
+        });
+        if (ahp) pn_small(ahp, ncol, ah, tag_of_tick(Cp), 1.f, sm.sah, P);
+        cons_sync(NCT);
+        if (stage_last && !loss_src && tid == 0) red_relaxed_sys(S.peer_g_credit, 1);  // gslot read
+        if (loss_src && P.loss == 1) {
+          // softmax cross-entropy: every CTA derives the whole delta in the
+          // same fixed order; CTA 0 records -log softmax[target]
+          float mx = -INFINITY;
+          for (int f = tid; f < P.F; f += NCT) mx = fmaxf(mx, sm.va[f]);
+          mx = pn_cta_red(mx, true, sm);
+          float se = 0.f;
+          for (int f = tid; f < P.F; f += NCT) se += expf(sm.va[f] - mx);
+          se = pn_cta_red(se, false, sm);
+          const float lse = mx + logf(se);
+          int tgt = -1;
+          bool ok = false;
+          if (y) {
+            tgt = int(y[0]);
+            ok = y[0] >= 0.f && y[0] < float(P.F) && float(tgt) == y[0];
+          }
+          if (c == 0 && tid == 0 && y) {
+            if (!ok) atomicMin(P.bad_target, sid);
+            P.loss_part[size_t(ti) * G] = ok ? lse - sm.va[tgt] : 0.f;
+          }
+          cons_sync(NCT);  // thread 0 read va[tgt] before it is rewritten
+          for (int f = tid; f < nout; f += NCT) {
+            const float a = sm.va[f];
+            sm.va[f] = (y && f < P.F) ? (expf(a - lse) - (f == tgt ? 1.f : 0.f)) * dact_fn(L.act, a) : 0.f;
+          }
+          cons_sync(NCT);
+        }
+        // the stage's last layer keeps its delta for the next tick (own forward rows); the bias step
+        for (int j = RB.r0 * PN_TS + tid; j < RB.r1 * PN_TS; j += NCT) {
+          const float d = sm.va[j];
+          if (stage_last) st_tv_gpu(L.dst + size_t(t & 1) * nout + j, pack_tv(d, tag_t));
+          if (upd_now && j < L.n_out) {
+            float* bp = sm.bias + sm.boff[S.first + i] + (j - RB.r0 * PN_TS);
+            *bp = fmaf(nlr, d, *bp);
+          }
+        }
+        PN_TR(13);
+        if (need_gin) {
+          const bool to_peer = (i == 0);  // first layer of stage h > 1: g_in goes upstream (no act')
+          const int act_prev = to_peer ? 0 : s_layers[S.first + i - 1].act;
+          for (int cb = CB.r0; cb < CB.r1; ++cb) {
+            // a_{l-1}(Ct) of the 16 published columns (rows of layer l-1), for act'
+            u64 ap = 0;
+            const u64* app = nullptr;
+            if (!to_peer && tid < PN_TS) {
+              app = Cc + L.cache_in + cb * PN_TS + tid;
+              ap = ld_tv_gpu(app);
+            }
+            const float4 ah4 = pend ? lds4(sm.sah + (cb - CB.r0) * PN_TS + f4 * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int j0 = 0; j0 < L.R; j0 += PN_CT) {
+              const int nt = min(PN_CT, L.R - j0);
+              const int slot = pn_take(sm, cslot, cphase, P);
+              PN_TRC(8);
+              const float* wb = sm.ring + size_t(slot) * PN_SLOT_FLOATS + toff;
+              const float* dl = sm.va + j0 * PN_TS + tr;
+              const float* sp = sm.vb + j0 * PN_TS + tr;
+              if (pend) {
+                if (nt == PN_CT) pn_bchunk<true, true>(wb, dl, sp, ah4, nt, tg, acc);
+                else pn_bchunk<true, false>(wb, dl, sp, ah4, nt, tg, acc);
+              } else {
+                if (nt == PN_CT) pn_bchunk<false, true>(wb, dl, sp, ah4, nt, tg, acc);
+                else pn_bchunk<false, false>(wb, dl, sp, ah4, nt, tg, acc);
+              }
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&sm.empty[slot]);
+            }
+            // column sums over tr (lane bits 2-4, warp bit 0) and tg (warp bits 1-2)
+            float g[4] = {acc.x, acc.y, acc.z, acc.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              g[e] += __shfl_xor_sync(0xffffffffu, g[e], 4);
+              g[e] += __shfl_xor_sync(0xffffffffu, g[e], 8);
+              g[e] += __shfl_xor_sync(0xffffffffu, g[e], 16);
+            }
+            float* rd = sm.red + ((cb - CB.r0) & 1) * 128;
+            if (lane < 4) {
+#pragma unroll
+              for (int e = 0; e < 4; ++e) rd[warp * PN_TS + lane * 4 + e] = g[e];
+            }
+            cons_sync(NCT);
+            if (tid < PN_TS) {
+              float o = 0.f;
+#pragma unroll
+              for (int w = 0; w < NCW; ++w) o += rd[w * PN_TS + tid];
+              const int col = cb * PN_TS + tid;
+              if (to_peer) {
+                const u64 wv = pack_tv(o, tag_t);
+                if (cb == CB.r0) {
+                  if (tid == 0) pn_wait_cnt(S.g_credit, u64(S.G_up) * u64(t), P);  // upstream read slot t&1 at t-1
+                  __syncwarp(0xffffu);
+                }
+                if (S.up_remote) st_tv_sys(S.peer_gslot[t & 1] + col, wv);
+                else st_tv_gpu(S.peer_gslot[t & 1] + col, wv);
+              } else {
+                // delta of layer l-1: g_in * act'(a_{l-1}(Ct)) (padding columns: g_in = 0)
+                const float av = pn_resolve(app, ap, tag_of_tick(Ct), false, P);
+                st_tv_gpu(L.gin[t & 1] + col, pack_tv(o * dact_fn(act_prev, av), tag_t));
+              }
+            }
+          }
+        }
+        if (!need_gin || CB.r0 == CB.r1) cons_sync(NCT);  // no chunk loop: the delta store's reads of va are done
+        PN_TR(14);
+      }
+    }
+    // end of tick: weight stores fenced for every producer's next-tick loads, then the tick
+    // barrier arrival
+    if (P.learn) fence_proxy_async_global();
+    cons_sync(NCT);
+    if (tid == 0) red_release_gpu(P.tick_end, 1);
+    PN_TR(20);
+  }
+#undef PN_TR
+#undef PN_TRC
+  if (P.learn && P.lr != 0.f) {
+    cons_sync(NCT);
+    for (int l = 0; l < P.n_layers; ++l) {
+      const PLayer& L = s_layers[l];
+      const Rows RB = rows_of(L.R, c, G);
+      for (int j = tid; j < (RB.r1 - RB.r0) * PN_TS; j += NCT) {
+        const int row = RB.r0 * PN_TS + j;
+        if (row < L.n_out) L.b[row] = sm.bias[sm.boff[l] + j];
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// layout conversion (pt_set_params / pt_get_params)
+// ---------------------------------------------------------------------------
+// row-major [n_out][n_in] -> tiled (zero padding)
+__global__ void pn_to_tiles(const float* __restrict__ src, float* __restrict__ dst, int n_out, int n_in, int R,
+                            int C) {
+  const size_t total = size_t(R) * C * PN_TILE;
+  for (size_t e = blockIdx.x * size_t(blockDim.x) + threadIdx.x; e < total; e += size_t(gridDim.x) * blockDim.x) {
+    const size_t tile = e / PN_TILE;
+    const int inner = int(e % PN_TILE);
+    const int rb = int(tile / C), cb = int(tile % C);
+    const int row = rb * PN_TS + inner / PN_TS, col = cb * PN_TS + inner % PN_TS;
+    dst[e] = (row < n_out && col < n_in) ? src[size_t(row) * n_in + col] : 0.f;
+  }
+}
+// tiled -> row-major, with the pending update of the last tick applied when sdel != null:
+// w + (-lr * delta[row]) * a_hat[col], the exact fmaf the next forward would apply
+__global__ void pn_from_tiles(const float* __restrict__ src, float* __restrict__ dst, int n_out, int n_in, int C,
+                              const u64* sdel, const u64* ahat, float lr) {
+  const size_t total = size_t(n_out) * n_in;
+  for (size_t e = blockIdx.x * size_t(blockDim.x) + threadIdx.x; e < total; e += size_t(gridDim.x) * blockDim.x) {
+    const int row = int(e / n_in), col = int(e % n_in);
+    float w = src[(size_t(row / PN_TS) * C + col / PN_TS) * PN_TILE + (row % PN_TS) * PN_TS + col % PN_TS];
+    if (sdel) w = fmaf(-lr * tv_val(sdel[row]), tv_val(ahat[col]), w);
+    dst[e] = w;
+  }
+}
+
+}  // namespace pt

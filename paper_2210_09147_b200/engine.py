@@ -337,11 +337,12 @@ class Pipeline:
 
     @property
     def kernel_path(self):
-        """'tile' (tcgen05 tensor-core tile kernel, batch 16) or 'tick' (per-row SIMT kernel)."""
+        """'panel' (batch-1 SGD panel kernel), 'tile' (tcgen05 tensor-core tile kernel, batch 16)
+        or 'tick' (row-owned SIMT tick kernel, every other case)."""
         r = self._lib.pt_kernel_path(self._h)
         if r < 0:
             _lib.check(r, "kernel_path")
-        return "tile" if r == 1 else "tick"
+        return {0: "tick", 1: "tile", 2: "panel"}[r]
 
     def last_kernel_ms(self):
         ms = ctypes.c_float()
