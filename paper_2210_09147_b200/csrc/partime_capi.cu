@@ -120,7 +120,7 @@ struct LayerHost {
   int R = 0, C = 0;
   float* Wt[2] = {nullptr, nullptr};
   u64* gin[2] = {nullptr, nullptr};
-  u64* dst = nullptr;
+  float* dpl = nullptr;
   long long set_tick = 0;
 };
 
@@ -130,7 +130,8 @@ struct StageHost {
   int first_local = 0;          // index into the handle's layer array
   int ld0 = 0, ldk = 0;
   char* comm = nullptr;  // own comm block
-  u64* cache = nullptr;  // 3 slots of tagged activations
+  u64* cache = nullptr;  // 3 slots of tagged activations (4 on the panel path)
+  float* pcache = nullptr;  // panel path: plain copies of the 4 slots
   size_t cache_words = 0;
   char* up = nullptr;    // upstream stage's comm block (local or IPC-mapped), h > 1
   char* down = nullptr;  // downstream stage's comm block, h < D
@@ -597,14 +598,7 @@ int upload_panel_desc(pt_pipeline* p) {
       d.gin[j] = h.gin[j];
     }
     d.b = h.b;
-    d.dst = h.dst;
-    if (h.dst) {
-      d.dsrc = h.dst;
-      d.dsrc_stride = h.R * pt::PN_TS;
-    } else if (i + 1 < p->layers.size()) {
-      d.dsrc = p->layers[i + 1].gin[0];
-      d.dsrc_stride = p->layers[i + 1].C * pt::PN_TS;
-    }
+    d.dpl = h.dpl;
     d.n_in = h.n_in;
     d.n_out = h.n_out;
     d.R = h.R;
@@ -629,7 +623,10 @@ int upload_panel_desc(pt_pipeline* p) {
     d.down_remote = h.down_remote ? 1 : 0;
     d.ld0 = h.ld0;
     d.ldk = h.ldk;
-    for (int j = 0; j < 4; ++j) d.cache[j] = h.cache + size_t(j) * h.cache_words;
+    for (int j = 0; j < 4; ++j) {
+      d.cache[j] = h.cache + size_t(j) * h.cache_words;
+      d.pcache[j] = h.pcache + size_t(j) * h.cache_words;
+    }
     const CommLayout own = p->layout_of(s0);
     for (int j = 0; j < 2; ++j) {
       d.inslot[j] = reinterpret_cast<u64*>(h.comm + own.inslot(j));
@@ -697,15 +694,12 @@ int setup_panel(pt_pipeline* p) {
     maxcoln = std::max(maxcoln, (Lh.C + G - 1) / G * pt::PN_TS);
     const int li_global = p->layer_base + int(i);
     if (p->learn) {
-      // a stage's last layer keeps its own delta [2][R*16]; every other layer's delta is the next
-      // layer's published vector gin [2][C*16] (both tick parities in one block)
-      const int h = stage_of_layer(p, li_global);
-      if (li_global + 1 == p->sfl[h])
-        PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&Lh.dst), size_t(2) * Lh.R * pt::PN_TS * sizeof(u64)));
-      if (li_global != 0) {
-        PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&Lh.gin[0]), size_t(2) * Lh.C * pt::PN_TS * sizeof(u64)));
-        Lh.gin[1] = Lh.gin[0] + size_t(Lh.C) * pt::PN_TS;
-      }
+      // delta (plain copy, read one tick later) [2][R*16]; the tagged delta of the previous
+      // layer this layer's backward publishes [2][C*16]
+      PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&Lh.dpl), size_t(2) * Lh.R * pt::PN_TS * sizeof(float)));
+      if (li_global != 0)
+        for (int j = 0; j < 2; ++j)
+          PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&Lh.gin[j]), size_t(Lh.C) * pt::PN_TS * sizeof(u64)));
     }
   }
   if (p->learn) {
@@ -719,13 +713,15 @@ int setup_panel(pt_pipeline* p) {
   }
   PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&p->d_players), p->layers.size() * sizeof(pt::PLayer)));
   PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&p->d_pstages), p->stages.size() * sizeof(pt::PStage)));
+  for (StageHost& S : p->stages)
+    PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&S.pcache), 4 * S.cache_words * sizeof(float)));
   // shared memory: ring (32 KB slots) first, then the vectors and small buffers
   auto a128 = [](size_t v) { return int(align_up(v, 128)); };
   const int desc = a128(p->layers.size() * sizeof(pt::PLayer) + p->stages.size() * sizeof(pt::PStage) +
-                        p->layers.size() * sizeof(int));
+                        p->layers.size() * 7 * sizeof(int));  // + bias offsets and block ranges
   const int bias = a128(bias_rows * 4);
   const int tail = 2 * a128(size_t(maxw) * 4) + a128(size_t(maxrown) * 4) + a128(size_t(maxcoln) * 4) +
-                   a128((256 + 64) * 4) + a128(2 * pt::PN_MAXSLOT * 8) + desc + bias;
+                   a128((256 + 64) * 4) + a128(3 * pt::PN_MAXSLOT * 8) + desc + bias;
   const int slot_bytes = pt::PN_SLOT_FLOATS * 4;
   int nslot = std::min(pt::PN_MAXSLOT, (pt::SMEM_MAX - tail) / slot_bytes);
   if (const char* e = getenv("PT_NSLOT")) nslot = std::min(nslot, std::max(2, atoi(e)));
@@ -744,7 +740,7 @@ int setup_panel(pt_pipeline* p) {
   p->pn_red = off;
   off += a128((256 + 64) * 4);
   p->pn_bar = off;
-  off += a128(2 * pt::PN_MAXSLOT * 8);
+  off += a128(3 * pt::PN_MAXSLOT * 8);
   p->pn_desc = off;
   off += desc;
   p->pn_bias = off;
@@ -1235,6 +1231,8 @@ int run_impl(pt_pipeline* p, const float* xs, const float* ys, int64_t n, float*
     Q.desc_off = p->pn_desc;
     Q.bias_off = p->pn_bias;
     Q.pf_chunks = p->pn_pf;
+    Q.psleep = getenv("PT_PSLEEP") ? atoi(getenv("PT_PSLEEP")) : 0;
+    Q.dbg = getenv("PT_PN_DBG") ? atoi(getenv("PT_PN_DBG")) : 0;
     Q.policy = p->policy;
     Q.trace = p->d_trace;
     Q.trace_cap = p->trace_cap;
@@ -1420,15 +1418,13 @@ int pt_get_params(pt_pipeline* p, int32_t layer, float* W, float* b, int32_t whe
       const long long T = p->t_next;
       const int h = stage_of_layer(p, layer);
       const bool pend = p->learn && p->lr != 0.f && T - 1 >= 2LL * p->D - h - 1 && T - 1 >= Lh->set_tick;
-      const u64* sdel = nullptr;
-      const u64* ahat = nullptr;
+      const float* sdel = nullptr;
+      const float* ahat = nullptr;
       if (pend) {
         const StageHost& S = p->stages[h - 1 - p->local_first];
         const long long Cp = (h < p->D && p->act_delay) ? T - 2 : T - 1;
-        const size_t li = size_t(layer - p->layer_base);
-        sdel = Lh->dst ? Lh->dst + size_t((T - 1) & 1) * Lh->R * pt::PN_TS
-                       : p->layers[li + 1].gin[0] + size_t((T - 1) & 1) * p->layers[li + 1].C * pt::PN_TS;
-        ahat = S.cache + size_t(Cp & 3) * S.cache_words + Lh->cache_in;
+        sdel = Lh->dpl + size_t((T - 1) & 1) * Lh->R * pt::PN_TS;
+        ahat = S.pcache + size_t(Cp & 3) * S.cache_words + Lh->cache_in;
       }
       const size_t nw = size_t(Lh->n_out) * Lh->n_in;
       PT_TRY(panel_rowbuf(p, nw));

@@ -59,9 +59,7 @@ struct PLayer {
   const CUtensorMap* tm[2];  // 3-D maps {256 floats, C, R} of W[0] / W[1]: column-panel boxes of 32 tiles
   float* b;                  // bias [n_out] (the owner CTA keeps its rows in smem during a launch)
   u64* gin[2];               // tagged delta of the previous layer = act' * g_in, [C*16] per tick parity
-  u64* dst;                  // stage's last layer: tagged delta [2][R*16] per tick parity
-  const u64* dsrc;           // this layer's delta vector [2][R*16]: the next layer's gin or dst
-  int dsrc_stride;           // words between the two parities of dsrc
+  float* dpl;                // plain copy of this layer's delta, [2][R*16] per tick parity (read at t+1)
   int n_in, n_out, R, C, act;
   int cache_in, cache_out;   // word offsets of a_{l-1}, a_l in a stage cache slot
   long long set_tick;        // pt_set_params at this tick discarded the pending update of earlier ticks
@@ -72,6 +70,7 @@ struct PStage {
   int G_up, G_down, up_remote, down_remote;
   int ld0, ldk;              // stage slot strides (words)
   u64* cache[4];             // tagged activation cache slots, tick mod 4
+  float* pcache[4];          // plain copies (read one tick or more later: a_hat, act')
   u64* inslot[2];
   u64* gslot[2];
   u64* peer_inslot[2];
@@ -103,6 +102,8 @@ struct PParams {
   int nslot, va_off, vb_off, sown_off, sah_off, red_off, bar_off, desc_off, bias_off;
   int policy;
   int pf_chunks;    // L2 prefetch distance of the producer (chunks)
+  int psleep;       // producer spin back-off (ns)
+  int dbg;          // experiments: bit0 = no per-step store fence, bit1 = no update-ahead
   u64* trace;
   int trace_cap, trace_cta;
   int jitter, jitter_mask;
@@ -115,7 +116,7 @@ __device__ __forceinline__ bool pn_upd(const PParams& P, int h, long long t) {
 }
 // the update of tick t-1 is still to be applied to layer L at tick t
 __device__ __forceinline__ bool pn_pending(const PParams& P, const PLayer& L, int h, long long t) {
-  return pn_upd(P, h, t - 1) && t - 1 >= L.set_tick;
+  return pn_upd(P, h, t - 1) && t - 1 >= L.set_tick && !(P.dbg & 8);
 }
 // the cache tick whose activations B(t) uses (act_delay reading)
 __device__ __forceinline__ long long pn_ct(const PParams& P, int h, long long t) {
@@ -187,6 +188,31 @@ __device__ __forceinline__ void pn_small(const u64* p, int n, u64 v0, uint32_t t
     dst[j] = scale * pn_resolve(p + j, v, tag, false, P);
   }
 }
+
+// A plain fp32 vector written in an earlier tick (visible after the tick barrier), loaded by the
+// consumer threads into registers first (issue, together with a step's other loads) and put
+// into shared memory later (store). Words [0, 2048) take one round trip.
+struct PPlain {
+  float4 v[2];
+  __device__ __forceinline__ void issue(const float* p, int n) {
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int j = int(threadIdx.x) * 4 + NCT * 4 * q;
+      v[q] = j < n ? ldcg4(reinterpret_cast<const float4*>(p + j)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+  __device__ __forceinline__ void store(const float* p, int n, float scale, float* dst) {
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int j = int(threadIdx.x) * 4 + NCT * 4 * q;
+      if (j < n) *reinterpret_cast<float4*>(dst + j) = make_float4(scale * v[q].x, scale * v[q].y, scale * v[q].z, scale * v[q].w);
+    }
+    for (int j = int(threadIdx.x) * 4 + NCT * 8; j < n; j += NCT * 4) {
+      const float4 u = ldcg4(reinterpret_cast<const float4*>(p + j));
+      *reinterpret_cast<float4*>(dst + j) = make_float4(scale * u.x, scale * u.y, scale * u.z, scale * u.w);
+    }
+  }
+};
 
 struct PV {
   const u64* p;  // null: not gathered (values read as 0)
@@ -287,6 +313,7 @@ __device__ __forceinline__ void pn_tma_prefetch_3d(const CUtensorMap* tm, int c0
 // [F_0..F_{k-1}, B_{k-1}..B_0] x own blocks x chunks); backward steps without weight reads
 // (stage 1, layer 0) have no chunks. fstep counts forward steps from the launch start.
 struct PCursor {
+  const int* tbl;           // per-layer block ranges of this CTA (PSmem::blk)
   int ti, s, st, blk, off;  // tick, stage, step, own block, chunk offset (tiles) in the block
   int b0, b1, len, nsteps, k, fstep;
   bool done;
@@ -299,11 +326,12 @@ struct PCursor {
     const int i = st < S.k ? st : 2 * S.k - 1 - st;
     L = &layers[S.first + i];
     Rows R;
+    const int* b = tbl + 6 * (S.first + i);
     if (st < S.k) {
-      R = rows_of(L->R, blockIdx.x, P.G);
+      R = Rows{b[0], b[1]};
       len = L->C;
     } else {
-      R = (S.h == 1 && i == 0) ? Rows{0, 0} : rows_of(L->C, blockIdx.x, P.G);
+      R = (S.h == 1 && i == 0) ? Rows{0, 0} : Rows{b[2], b[3]};
       len = L->R;
     }
     b0 = R.r0;
@@ -348,16 +376,20 @@ struct PCursor {
   __device__ __forceinline__ size_t foff() const { return (size_t(blk) * L->C + off) * PN_TILE; }
 };
 
-// fwd_fenced: forward steps whose consumer weight stores are fenced for the async proxy
-// (count from the launch start, written by consumer thread 0)
+// Weight write-back is the consumers' (st.global from registers, fenced for the async proxy).
+// The producer issues a tick's forward loads of its own rows once its consumers have fenced
+// the previous tick's stores of that layer (fwd_fenced: forward steps fenced, counted from the
+// launch start), and a tick's backward loads (column panels holding every CTA's stores) once
+// every CTA finished the previous tick.
 __device__ void pn_producer(const PParams& P, const PLayer* layers, const PStage* stages, float* ring,
-                            uint64_t* full, uint64_t* empty, const int* fwd_fenced, int nF) {
+                            uint64_t* full, uint64_t* empty, const int* fwd_fenced, int nF, const int* tbl) {
   const uint64_t pol = P.policy == 1 ? policy_evict_normal() : policy_evict_first();
   const int G = P.G, nslot = P.nslot;
   uint32_t chunk = 0;
   bool dead = false;
   int tr = P.trace_cap / 2;
   PCursor cur, pf;
+  cur.tbl = pf.tbl = tbl;
   cur.init(P, stages, layers);
   pf.init(P, stages, layers);
   uint32_t pf_idx = 0;
@@ -380,12 +412,12 @@ __device__ void pn_producer(const PParams& P, const PLayer* layers, const PStage
     const long long t = cur.t(P);
     if (P.learn && ti > 0) {
       if (cur.fwd()) {
-        // my rows of this layer were stored by my consumers at tick ti-1: fenced yet?
-        const int need = cur.fstep - nF + 1;
+        const int need = cur.fstep - nF + 1;  // the same layer's forward step of tick ti-1
         if (ld_acquire_cta_s32(fwd_fenced) < need) {
           const uint64_t t0 = globaltimer();
           while (ld_acquire_cta_s32(fwd_fenced) < need) {
             top_up();
+            if (P.psleep) __nanosleep(P.psleep);
             if (pn_watchdog(P, t0)) {
               dead = true;
               break;
@@ -393,7 +425,6 @@ __device__ void pn_producer(const PParams& P, const PLayer* layers, const PStage
           }
         }
       } else if (ti > raw_ti) {
-        // column panels hold every CTA's tick ti-1 stores
         pn_wait_cnt(P.tick_end, u64(G) * u64(t), P);
         fence_proxy_async_global();
         raw_ti = ti;
@@ -405,6 +436,7 @@ __device__ void pn_producer(const PParams& P, const PLayer* layers, const PStage
       const uint64_t t0 = globaltimer();
       while (!dead && !mbar_try_wait(&empty[slot], (use - 1) & 1u)) {
         top_up();
+        if (P.psleep) __nanosleep(P.psleep);  // leave issue slots to the consumer warps of this SMSP
         if (pn_watchdog(P, t0)) dead = true;
       }
     }
@@ -446,7 +478,8 @@ struct PSmem {
   float* scal;  // 64 floats
   float* bias;  // own forward rows of every local layer's bias, resident for the launch
   int* boff;    // per layer: offset of its rows in `bias`
-  int* flags;   // [0] forward steps fenced (producer's RAW wait)
+  int* blk;     // per layer: this CTA's row blocks [0, 1), column blocks [2, 3), input words [4, 5)
+  int* flags;   // [0] forward steps whose weight stores are fenced (producer's RAW wait)
   uint64_t* full;
   uint64_t* empty;
 };
@@ -458,52 +491,55 @@ __device__ __forceinline__ void pn_fma4(float4& w, float s, float4 a) {
   w.w = fmaf(s, a.w, w.w);
 }
 
-// Forward chunk, update half: W^(t) = W^(t-1) + sc * a_hat (pending) on this thread's 8 tile
-// rows, written back into the slot (for the dot) and to the next buffer (HBM). All loads of a
-// batch are issued before any store.
+// Forward thread mapping: thread (f4, rg, tg) = (tid & 3, (tid >> 2) & 3, tid >> 4) takes
+// float4 f4 of rows rg + 4r (r < 4) of tiles tg and tg + 16 of a chunk, so one load of the
+// input vector serves four weight loads (a 128-bit shared load costs four crossbar phases even
+// when it is a broadcast). A quarter warp reads two whole consecutive tile rows (128 B).
+// Update half: W^(t) = W^(t-1) + sc[r] * a_hat, into the slot (for the dot) and to buffer t&1.
 template <bool PEND, bool FULL>
-__device__ __forceinline__ void pn_fupdate(float* wb, float* gdst, const float* vb, float sc, int nt, int tg) {
+__device__ __forceinline__ void pn_fupdate(float* wb, float* gdst, const float* vb, const float (&sc)[4], int nt,
+                                           int tg, bool nostore = false) {
+  float4 w[2][4], ah[2];
 #pragma unroll
-  for (int hb = 0; hb < 2; ++hb) {
-    float4 w[4], ah[4];
+  for (int q = 0; q < 2; ++q) {
+    const int tt = tg + 16 * q;
+    const bool ok = FULL || tt < nt;
+    ah[q] = (PEND && ok) ? lds4(vb + tt * PN_TS) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int tt = (hb * 4 + q) * 4 + tg;
-      const bool ok = FULL || tt < nt;
-      w[q] = ok ? lds4(wb + tt * PN_TILE) : make_float4(0.f, 0.f, 0.f, 0.f);
-      if (PEND) ah[q] = ok ? lds4(vb + tt * PN_TS) : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
+    for (int r = 0; r < 4; ++r) w[q][r] = ok ? lds4(wb + tt * PN_TILE + r * 64) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int tt = (hb * 4 + q) * 4 + tg;
-      if (PEND) pn_fma4(w[q], sc, ah[q]);
-      if (FULL || tt < nt) {
-        if (PEND) *reinterpret_cast<float4*>(wb + tt * PN_TILE) = w[q];
-        __stcs(reinterpret_cast<float4*>(gdst + tt * PN_TILE), w[q]);
+  for (int q = 0; q < 2; ++q) {
+    const int tt = tg + 16 * q;
+    if (FULL || tt < nt) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        if (PEND) {
+          pn_fma4(w[q][r], sc[r], ah[q]);
+          *reinterpret_cast<float4*>(wb + tt * PN_TILE + r * 64) = w[q][r];
+        }
+        if (!nostore) __stcs(reinterpret_cast<float4*>(gdst + tt * PN_TILE + r * 64), w[q][r]);
       }
     }
   }
 }
 
-// Forward chunk, dot half: this thread's partial of row tr over its 8 tiles (two accumulators,
-// fixed combination order)
+// Dot half: z[r] += W[row rg + 4r][this thread's columns] . a (fixed order)
 template <bool FULL>
-__device__ __forceinline__ float pn_fdot(const float* wb, const float* va, int nt, int tg) {
-  float4 w[8], a[8];
+__device__ __forceinline__ void pn_fdot(const float* wb, const float* va, int nt, int tg, float (&z)[4]) {
+  float4 w[2][4], a[2];
 #pragma unroll
-  for (int p = 0; p < 8; ++p) {
-    const int tt = p * 4 + tg;
+  for (int q = 0; q < 2; ++q) {
+    const int tt = tg + 16 * q;
     const bool ok = FULL || tt < nt;
-    w[p] = ok ? lds4(wb + tt * PN_TILE) : make_float4(0.f, 0.f, 0.f, 0.f);
-    a[p] = ok ? lds4(va + tt * PN_TS) : make_float4(0.f, 0.f, 0.f, 0.f);
-  }
-  float z0 = 0.f, z1 = 0.f;
+    a[q] = ok ? lds4(va + tt * PN_TS) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-  for (int p = 0; p < 8; p += 2) {
-    z0 += dot4(w[p], a[p]);
-    z1 += dot4(w[p + 1], a[p + 1]);
+    for (int r = 0; r < 4; ++r) w[q][r] = ok ? lds4(wb + tt * PN_TILE + r * 64) : make_float4(0.f, 0.f, 0.f, 0.f);
   }
-  return z0 + z1;
+#pragma unroll
+  for (int q = 0; q < 2; ++q)
+#pragma unroll
+    for (int r = 0; r < 4; ++r) z[r] += dot4(w[q][r], a[q]);
 }
 
 // Backward chunk: acc += W^(t)[rows][own 4 columns] * delta[rows], W^(t) rebuilt from the
@@ -588,6 +624,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constan
   PLayer* s_layers = reinterpret_cast<PLayer*>(smem_raw + P.desc_off);
   PStage* s_stages = reinterpret_cast<PStage*>(s_layers + P.n_layers);
   sm.boff = reinterpret_cast<int*>(s_stages + P.n_stages);
+  sm.blk = sm.boff + P.n_layers;
   sm.bias = reinterpret_cast<float*>(smem_raw + P.bias_off);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -611,18 +648,29 @@ __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constan
   __syncthreads();
   int nF = 0;  // forward steps per tick
   for (int s = 0; s < P.n_stages; ++s) nF += s_stages[s].k;
+  for (int l = tid; l < P.n_layers; l += NTHREADS) {  // block ranges (no divisions in the tick loop)
+    const Rows RB = rows_of(s_layers[l].R, c, G), CB = rows_of(s_layers[l].C, c, G);
+    const Rows Q = rows_of(s_layers[l].C * PN_TS, c, G);
+    int* b = sm.blk + 6 * l;
+    b[0] = RB.r0;
+    b[1] = RB.r1;
+    b[2] = CB.r0;
+    b[3] = CB.r1;
+    b[4] = Q.r0;
+    b[5] = Q.r1;
+  }
+  __syncthreads();
   if (tid == 0) {
     int off = 0;
     for (int l = 0; l < P.n_layers; ++l) {
       sm.boff[l] = off;
-      const Rows RB = rows_of(s_layers[l].R, c, G);
-      off += (RB.r1 - RB.r0) * PN_TS;
+      off += (sm.blk[6 * l + 1] - sm.blk[6 * l]) * PN_TS;
     }
   }
   __syncthreads();
   for (int l = 0; l < P.n_layers; ++l) {
     const PLayer& L = s_layers[l];
-    const Rows RB = rows_of(L.R, c, G);
+    const Rows RB{sm.blk[6 * l], sm.blk[6 * l + 1]};
     for (int j = tid; j < (RB.r1 - RB.r0) * PN_TS; j += NTHREADS) {
       const int row = RB.r0 * PN_TS + j;
       sm.bias[sm.boff[l] + j] = row < L.n_out ? L.b[row] : 0.f;
@@ -638,16 +686,19 @@ __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constan
           tma_fence_desc_acquire(s_layers[l].tm[b]);
           tma_prefetch_desc(s_layers[l].tm[b]);
         }
-      pn_producer(P, s_layers, s_stages, sm.ring, sm.full, sm.empty, sm.flags, nF);
+      pn_producer(P, s_layers, s_stages, sm.ring, sm.full, sm.empty, sm.flags, nF, sm.blk);
     }
     return;
   }
-  // thread's place in a chunk: float4 f4 of row tr of tiles tg, tg+4, ... (8 tiles of 32)
+  // backward: float4 f4 of row tr of tiles tg, tg+4, ... (8 tiles of a chunk); forward: see
+  // pn_fupdate (float4 f4 of rows fr + 4r of tiles fg, fg + 16)
   const int f4 = tid & 3, tr = (tid >> 2) & 15, tg = tid >> 6;
-  const int toff = tr * PN_TS + f4 * 4;  // this thread's float4 inside a tile
+  const int toff = tr * PN_TS + f4 * 4;  // this thread's float4 inside a tile (backward)
+  const int fr = (tid >> 2) & 3, fg = tid >> 4;
+  const int foff = fr * PN_TS + f4 * 4;  // forward: row fr of the tile, float4 f4
+  int fdone = 0;  // forward steps of this launch whose weight stores are issued
   int cslot = 0;        // ring slot of the next chunk
   uint32_t cphase = 0;  // its full-barrier phase parity
-  int fdone = 0;        // forward steps of this launch completed (their stores precede the next fence)
   int tri = 0;
   int trc = P.trace_cap - P.trace_cap / 4;  // chunk-ready events: last quarter of the trace buffer
   const int trl = P.trace_cap / 2;
@@ -674,6 +725,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constan
     if (tid == 0) {
       if (P.learn && t >= 1) pn_wait_cnt(P.tick_end, u64(G) * u64(t), P);
       else if (!P.learn && t >= 2) pn_wait_cnt(P.tick_end, u64(G) * u64(t - 1), P);
+      __threadfence();
     }
     for (int s = 0; s < P.n_stages; ++s) {
       const PStage& S = s_stages[s];
@@ -683,7 +735,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constan
       for (int i = 0; i < S.k; ++i) {
         const PLayer& L = s_layers[S.first + i];
         const int nin = L.C * PN_TS;
-        const Rows RB = rows_of(L.R, c, G);
+        const int* bk = sm.blk + 6 * (S.first + i);
+        const Rows RB{bk[0], bk[1]};
         const int nown = (RB.r1 - RB.r0) * PN_TS;
         const int nch = (L.C + PN_CT - 1) / PN_CT;  // chunks per row block
         const bool last = i == S.k - 1;
@@ -691,7 +744,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constan
         const long long Cp = pn_ct(P, h, t - 1);
         PN_TR(1);
         // every weight store of earlier forward steps is fenced for the producer's loads
-        if (P.learn) fence_proxy_async_global();
+        if (P.learn && !(P.dbg & 1)) fence_proxy_async_global();
         // the input vector (the dependency): loads in flight now, resolved after the update
         PV vin{nullptr, 0u, 0};
         if (i == 0 && h > 1) vin = PV{S.inslot[(t - 1) & 1], tag_of_tick(t - 1), S.up_remote};
@@ -699,14 +752,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constan
         PBatch dep;
         dep.issue(vin, nin, 0);
         if (pend) {
-          const u64* sop = L.dsrc + size_t((t - 1) & 1) * L.dsrc_stride + RB.r0 * PN_TS;
-          const u64 so = tid < nown ? ld_tv_gpu(sop + tid) : 0ull;
-          PV va1[1] = {PV{S.cache[cmod4(Cp)] + L.cache_in, tag_of_tick(Cp), 0}};
-          pn_gather<1>(va1, nin, P, [&](int j, const float (&x)[1][2]) {
-            sm.vb[j] = x[0][0];
-            sm.vb[j + 1] = x[0][1];
-          });
-          pn_small(sop, nown, so, tag_of_tick(t - 1), -P.lr, sm.sown, P);
+          // a_hat_{t-1} and delta_{t-1} of own rows: plain copies from earlier ticks, loaded
+          // together with the input's words
+          const float* ap = S.pcache[cmod4(Cp)] + L.cache_in;
+          const float* dp = L.dpl + size_t((t - 1) & 1) * (L.R * PN_TS) + RB.r0 * PN_TS;
+          PPlain ahr;
+          ahr.issue(ap, nin);
+          const float so = tid < nown ? ldcg(dp + tid) : 0.f;
+          ahr.store(ap, nin, 1.f, sm.vb);
+          if (tid < nown) sm.sown[tid] = -P.lr * so;
+          for (int j = tid + NCT; j < nown; j += NCT) sm.sown[j] = -P.lr * ldcg(dp + j);
         }
         cons_sync(NCT);
         if (P.learn && tid == 0) st_release_cta_s32(&sm.flags[0], fdone);
@@ -714,27 +769,29 @@ __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constan
         // update-ahead: the pending update of the chunks the ring can hold, before the input
         // is there; W^(t) goes to the slot and to buffer t&1
         const int nck = nch * (RB.r1 - RB.r0);
-        const int ua = P.learn ? min(nck, P.nslot) : 0;
+        const int ua = (P.learn && !(P.dbg & 2)) ? min(nck, P.nslot) : 0;
         float* Wn = L.W[int(t & 1)];
         {
           int k = 0;
           int us = cslot;
           uint32_t up = cphase;
           for (int rb = RB.r0; rb < RB.r1 && k < ua; ++rb) {
-            const float sc = pend ? sm.sown[(rb - RB.r0) * PN_TS + tr] : 0.f;
+            float sc[4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) sc[r] = pend ? sm.sown[(rb - RB.r0) * PN_TS + fr + 4 * r] : 0.f;
             for (int c0 = 0; c0 < L.C && k < ua; c0 += PN_CT, ++k) {
               const int nt = min(PN_CT, L.C - c0);
               const int slot = pn_take(sm, us, up, P);
               PN_TRC(7);
-              float* wb = sm.ring + size_t(slot) * PN_SLOT_FLOATS + toff;
-              float* gd = Wn + (size_t(rb) * L.C + c0) * PN_TILE + toff;
+              float* wb = sm.ring + size_t(slot) * PN_SLOT_FLOATS + foff;
+              float* gd = Wn + (size_t(rb) * L.C + c0) * PN_TILE + foff;
               const float* vb = sm.vb + c0 * PN_TS + f4 * 4;
               if (pend) {
-                if (nt == PN_CT) pn_fupdate<true, true>(wb, gd, vb, sc, nt, tg);
-                else pn_fupdate<true, false>(wb, gd, vb, sc, nt, tg);
+                if (nt == PN_CT) pn_fupdate<true, true>(wb, gd, vb, sc, nt, fg, (P.dbg & 4) != 0);
+                else pn_fupdate<true, false>(wb, gd, vb, sc, nt, fg, (P.dbg & 4) != 0);
               } else {
-                if (nt == PN_CT) pn_fupdate<false, true>(wb, gd, vb, sc, nt, tg);
-                else pn_fupdate<false, false>(wb, gd, vb, sc, nt, tg);
+                if (nt == PN_CT) pn_fupdate<false, true>(wb, gd, vb, sc, nt, fg, (P.dbg & 4) != 0);
+                else pn_fupdate<false, false>(wb, gd, vb, sc, nt, fg, (P.dbg & 4) != 0);
               }
             }
           }
@@ -767,8 +824,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constan
         cons_sync(NCT);
         if (i == 0) {
           // private copy of the stage input in the cache (inslot is rewritten at t+1)
-          const Rows Q = rows_of(nin, c, G);
-          for (int j = Q.r0 + tid; j < Q.r1; j += NCT) st_tv_gpu(Ccur + L.cache_in + j, pack_tv(sm.va[j], tag_t));
+          const Rows Q{bk[4], bk[5]};
+          float* pc = S.pcache[cmod4(t)] + L.cache_in;
+          for (int j = Q.r0 + tid; j < Q.r1; j += NCT) {
+            st_tv_gpu(Ccur + L.cache_in + j, pack_tv(sm.va[j], tag_t));
+            pc[j] = sm.va[j];
+          }
           if (h > 1 && tid == 0) red_relaxed_sys(S.peer_act_credit, 1);  // inslot read (all threads: cons_sync above)
         }
         PN_TR(3);
@@ -778,40 +839,55 @@ __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constan
         float lsum = 0.f;
         int k = 0;
         for (int rb = RB.r0; rb < RB.r1; ++rb) {
-          const float sc = pend ? sm.sown[(rb - RB.r0) * PN_TS + tr] : 0.f;
-          float z = 0.f;
+          float sc[4];
+#pragma unroll
+          for (int r = 0; r < 4; ++r) sc[r] = pend ? sm.sown[(rb - RB.r0) * PN_TS + fr + 4 * r] : 0.f;
+          float z[4] = {0.f, 0.f, 0.f, 0.f};
           for (int c0 = 0; c0 < L.C; c0 += PN_CT, ++k) {
             const int nt = min(PN_CT, L.C - c0);
             const int slot = pn_take(sm, cslot, cphase, P);
             if (k >= ua) PN_TRC(7);
-            float* wb = sm.ring + size_t(slot) * PN_SLOT_FLOATS + toff;
+            float* wb = sm.ring + size_t(slot) * PN_SLOT_FLOATS + foff;
             const float* va = sm.va + c0 * PN_TS + f4 * 4;
             if (k >= ua && P.learn) {
               // beyond the update-ahead window: update (and store) here
-              float* gd = Wn + (size_t(rb) * L.C + c0) * PN_TILE + toff;
+              float* gd = Wn + (size_t(rb) * L.C + c0) * PN_TILE + foff;
               const float* vb = sm.vb + c0 * PN_TS + f4 * 4;
-              if (pend) pn_fupdate<true, false>(wb, gd, vb, sc, nt, tg);
-              else pn_fupdate<false, false>(wb, gd, vb, sc, nt, tg);
+              if (pend) pn_fupdate<true, false>(wb, gd, vb, sc, nt, fg, (P.dbg & 4) != 0);
+              else pn_fupdate<false, false>(wb, gd, vb, sc, nt, fg, (P.dbg & 4) != 0);
             }
-            z += nt == PN_CT ? pn_fdot<true>(wb, va, nt, tg) : pn_fdot<false>(wb, va, nt, tg);
+            if (nt == PN_CT) pn_fdot<true>(wb, va, nt, fg, z);
+            else pn_fdot<false>(wb, va, nt, fg, z);
+            PN_TRC(9);
             __syncwarp();
             if (lane == 0) mbar_arrive(&sm.empty[slot]);
           }
-          z += __shfl_xor_sync(0xffffffffu, z, 1);
-          z += __shfl_xor_sync(0xffffffffu, z, 2);
+          // row rg + 4r: sum over f4 (lane bits 0-1) and fg (lane bit 4, then the warps)
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            z[r] += __shfl_xor_sync(0xffffffffu, z[r], 1);
+            z[r] += __shfl_xor_sync(0xffffffffu, z[r], 2);
+            z[r] += __shfl_xor_sync(0xffffffffu, z[r], 16);
+          }
           float* rd = sm.red + ((rb - RB.r0) & 1) * 128;
-          if (f4 == 0) rd[tg * PN_TS + tr] = z;
+          if ((lane & 19) == 0) {
+#pragma unroll
+            for (int r = 0; r < 4; ++r) rd[warp * PN_TS + fr + 4 * r] = z[r];
+          }
           cons_sync(NCT);
+          PN_TRC(10);
           if (tid < PN_TS) {
             const int row = rb * PN_TS + tid;
             float a = 0.f;
             if (row < L.n_out) {
-              const float zz = ((rd[tid] + rd[PN_TS + tid]) + rd[2 * PN_TS + tid]) + rd[3 * PN_TS + tid] +
-                               sm.bias[sm.boff[S.first + i] + (rb - RB.r0) * PN_TS + tid];
-              a = act_fn(L.act, zz);
+              float zz = 0.f;
+#pragma unroll
+              for (int w = 0; w < NCW; ++w) zz += rd[w * PN_TS + tid];
+              a = act_fn(L.act, zz + sm.bias[sm.boff[S.first + i] + (rb - RB.r0) * PN_TS + tid]);
             }
             const u64 w = pack_tv(a, tag_t);
             st_tv_gpu(Ccur + L.cache_out + row, w);
+            S.pcache[cmod4(t)][L.cache_out + row] = a;
             if (last && h < P.D) {
               if (rb == RB.r0) {
                 if (tid == 0) pn_wait_cnt(S.act_credit, u64(S.G_down) * u64(t), P);  // downstream read slot t&1 at t-1
@@ -871,8 +947,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constan
       for (int i = S.k - 1; i >= 0; --i) {
         const PLayer& L = s_layers[S.first + i];
         const int nout = L.R * PN_TS;
-        const Rows RB = rows_of(L.R, c, G);
-        const Rows CB = rows_of(L.C, c, G);
+        const int* bk = sm.blk + 6 * (S.first + i);
+        const Rows RB{bk[0], bk[1]};
+        const Rows CB{bk[2], bk[3]};
         const int ncol = (CB.r1 - CB.r0) * PN_TS;
         const bool need_gin = !(h == 1 && i == 0);
         const bool pend = pn_pending(P, L, h, t);
@@ -880,16 +957,20 @@ __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constan
         const bool stage_last = i == S.k - 1;
         const bool loss_src = stage_last && h == P.D;
         PN_TR(11);
-        // own columns' a_hat_{t-1}: issued now, resolved after the gather
-        u64 ah = 0;
-        const u64* ahp = nullptr;
-        if (pend && need_gin) {
-          ahp = S.cache[cmod4(Cp)] + L.cache_in + CB.r0 * PN_TS;
-          if (tid < ncol) ah = ld_tv_gpu(ahp + tid);
+        // pending update of tick t-1 (plain copies from earlier ticks): own columns' a_hat and
+        // -lr * delta_{t-1} of every row
+        // (loads issued here, stored after the gather below: one round trip for everything)
+        const float* sap = (pend && need_gin) ? S.pcache[cmod4(Cp)] + L.cache_in + CB.r0 * PN_TS : nullptr;
+        const float* sdp = (pend && need_gin) ? L.dpl + size_t((t - 1) & 1) * nout : nullptr;
+        PPlain dpr;
+        float sa = 0.f;
+        if (sdp) {
+          dpr.issue(sdp, nout);
+          if (tid < ncol) sa = ldcg(sap + tid);
         }
         // delta_l(t): the next layer's published vector, or (stage's last layer) the loss
         // gradient / the downstream stage's g_in times act'; delta_l(t-1) for the rebuild
-        PV vg[3];
+        PV vg[2];
         vg[0] = PV{nullptr, 0u, 0};
         vg[1] = PV{nullptr, 0u, 0};
         if (loss_src) {
@@ -898,15 +979,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constan
           vg[0] = PV{S.gslot[(t - 1) & 1], tag_of_tick(t - 1), S.down_remote};
           vg[1] = PV{Cc + L.cache_out, tag_of_tick(Ct), 0};
         } else {
-          vg[0] = PV{L.dsrc + size_t(t & 1) * L.dsrc_stride, tag_t, 0};
+          vg[0] = PV{s_layers[S.first + i + 1].gin[t & 1], tag_t, 0};
         }
-        vg[2] = (pend && need_gin) ? PV{L.dsrc + size_t((t - 1) & 1) * L.dsrc_stride, tag_of_tick(t - 1), 0}
-                                   : PV{nullptr, 0u, 0};
         const long long sid = t - (P.D - 1);
         const float* y = loss_src ? pn_target(P, sid, P.loss == 1 ? 1 : P.F) : nullptr;
         const float g_scale = 2.f / float(P.F);  // d mse / d a (M = 1)
         const float nlr = -P.lr;
-        pn_gather<3>(vg, nout, P, [&](int j, const float (&x)[3][2]) {
+        pn_gather<2>(vg, nout, P, [&](int j, const float (&x)[2][2]) {
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             float d;
@@ -920,10 +999,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constan
               d = x[0][e];
             }
             sm.va[j + e] = d;
-            sm.vb[j + e] = nlr * x[2][e];
           }
         });
-        if (ahp) pn_small(ahp, ncol, ah, tag_of_tick(Cp), 1.f, sm.sah, P);
+        if (sdp) {
+          dpr.store(sdp, nout, -P.lr, sm.vb);
+          if (tid < ncol) sm.sah[tid] = sa;
+          for (int j = tid + NCT; j < ncol; j += NCT) sm.sah[j] = ldcg(sap + j);
+        }
         cons_sync(NCT);
         if (stage_last && !loss_src && tid == 0) red_relaxed_sys(S.peer_g_credit, 1);  // gslot read
         if (loss_src && P.loss == 1) {
@@ -956,7 +1038,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constan
         // the stage's last layer keeps its delta for the next tick (own forward rows); the bias step
         for (int j = RB.r0 * PN_TS + tid; j < RB.r1 * PN_TS; j += NCT) {
           const float d = sm.va[j];
-          if (stage_last) st_tv_gpu(L.dst + size_t(t & 1) * nout + j, pack_tv(d, tag_t));
+          if (stage_last) L.dpl[size_t(t & 1) * nout + j] = d;
           if (upd_now && j < L.n_out) {
             float* bp = sm.bias + sm.boff[S.first + i] + (j - RB.r0 * PN_TS);
             *bp = fmaf(nlr, d, *bp);
@@ -965,7 +1047,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constan
         PN_TR(13);
         if (need_gin) {
           const bool to_peer = (i == 0);  // first layer of stage h > 1: g_in goes upstream (no act')
-          const int act_prev = to_peer ? 0 : s_layers[S.first + i - 1].act;
+          const PLayer* Lp = to_peer ? nullptr : &s_layers[S.first + i - 1];
           for (int cb = CB.r0; cb < CB.r1; ++cb) {
             // a_{l-1}(Ct) of the 16 published columns (rows of layer l-1), for act'
             u64 ap = 0;
@@ -1023,7 +1105,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constan
               } else {
                 // delta of layer l-1: g_in * act'(a_{l-1}(Ct)) (padding columns: g_in = 0)
                 const float av = pn_resolve(app, ap, tag_of_tick(Ct), false, P);
-                st_tv_gpu(L.gin[t & 1] + col, pack_tv(o * dact_fn(act_prev, av), tag_t));
+                const float d = o * dact_fn(Lp->act, av);
+                st_tv_gpu(L.gin[t & 1] + col, pack_tv(d, tag_t));
+                Lp->dpl[size_t(t & 1) * (Lp->R * PN_TS) + col] = d;  // for tick t+1
               }
             }
           }
@@ -1032,11 +1116,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constan
         PN_TR(14);
       }
     }
-    // end of tick: weight stores fenced for every producer's next-tick loads, then the tick
-    // barrier arrival
+    // end of tick: the tick barrier arrival (this tick's plain stores, and its weight stores
+    // fenced for the producers' TMA loads, are published with it)
     if (P.learn) fence_proxy_async_global();
     cons_sync(NCT);
-    if (tid == 0) red_release_gpu(P.tick_end, 1);
+    if (tid == 0) {
+      __threadfence();
+      red_release_gpu(P.tick_end, 1);
+    }
     PN_TR(20);
   }
 #undef PN_TR
@@ -1045,7 +1132,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constan
     cons_sync(NCT);
     for (int l = 0; l < P.n_layers; ++l) {
       const PLayer& L = s_layers[l];
-      const Rows RB = rows_of(L.R, c, G);
+      const Rows RB{sm.blk[6 * l], sm.blk[6 * l + 1]};
       for (int j = tid; j < (RB.r1 - RB.r0) * PN_TS; j += NCT) {
         const int row = RB.r0 * PN_TS + j;
         if (row < L.n_out) L.b[row] = sm.bias[sm.boff[l] + j];
@@ -1072,12 +1159,12 @@ __global__ void pn_to_tiles(const float* __restrict__ src, float* __restrict__ d
 // tiled -> row-major, with the pending update of the last tick applied when sdel != null:
 // w + (-lr * delta[row]) * a_hat[col], the exact fmaf the next forward would apply
 __global__ void pn_from_tiles(const float* __restrict__ src, float* __restrict__ dst, int n_out, int n_in, int C,
-                              const u64* sdel, const u64* ahat, float lr) {
+                              const float* sdel, const float* ahat, float lr) {
   const size_t total = size_t(n_out) * n_in;
   for (size_t e = blockIdx.x * size_t(blockDim.x) + threadIdx.x; e < total; e += size_t(gridDim.x) * blockDim.x) {
     const int row = int(e / n_in), col = int(e % n_in);
     float w = src[(size_t(row / PN_TS) * C + col / PN_TS) * PN_TILE + (row % PN_TS) * PN_TS + col % PN_TS];
-    if (sdel) w = fmaf(-lr * tv_val(sdel[row]), tv_val(ahat[col]), w);
+    if (sdel) w = fmaf(-lr * sdel[row], ahat[col], w);
     dst[e] = w;
   }
 }

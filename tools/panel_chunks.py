@@ -52,6 +52,16 @@ def main():
             if rs:
                 stats[kind].append((tg - tb, [r - tg for r in rs], [r - i for r, i in zip(rs, iss)],
                                     [tb - i for i in iss], t - rs[-1]))
+    # dot phase: ready (7) -> dot done (9) per chunk, and the reduction barrier (10)
+    ev = [(c, t) for c, t in chunks if c in (7, 9, 10)]
+    d9, d10 = [], []
+    for (c0, t0), (c1, t1) in zip(ev, ev[1:]):
+        if c1 == 9:
+            d9.append(t1 - t0)
+        if c1 == 10 and c0 == 9:
+            d10.append(t1 - t0)
+    if d9:
+        print(f"dot: median gap before each dot-done {np.median(d9) / 1e3:.2f}us; last dot -> reduction barrier {np.median(d10) / 1e3:.2f}us")
     for kind in ("F", "B"):
         v = stats[kind][len(stats[kind]) // 4:]
         if not v:
