@@ -122,6 +122,7 @@ struct LayerHost {
   u64* gin[2] = {nullptr, nullptr};
   float* dpl = nullptr;
   long long set_tick = 0;
+  int bw = 0;  // learning and the backward reads W: the backward applies the update (pt_panel.cuh)
 };
 
 struct StageHost {
@@ -599,6 +600,7 @@ int upload_panel_desc(pt_pipeline* p) {
     }
     d.b = h.b;
     d.dpl = h.dpl;
+    d.bw = h.bw;
     d.n_in = h.n_in;
     d.n_out = h.n_out;
     d.R = h.R;
@@ -694,10 +696,13 @@ int setup_panel(pt_pipeline* p) {
     maxcoln = std::max(maxcoln, (Lh.C + G - 1) / G * pt::PN_TS);
     const int li_global = p->layer_base + int(i);
     if (p->learn) {
-      // delta (plain copy, read one tick later) [2][R*16]; the tagged delta of the previous
-      // layer this layer's backward publishes [2][C*16]
-      PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&Lh.dpl), size_t(2) * Lh.R * pt::PN_TS * sizeof(float)));
-      if (li_global != 0)
+      // every layer but the network's first reads W in the backward and updates it there; the
+      // first layer's update is deferred to the next forward, which needs its delta a tick later
+      // (plain [2][R*16]). gin: the tagged delta of the previous layer this backward publishes.
+      Lh.bw = li_global != 0;
+      if (!Lh.bw)
+        PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&Lh.dpl), size_t(2) * Lh.R * pt::PN_TS * sizeof(float)));
+      else
         for (int j = 0; j < 2; ++j)
           PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&Lh.gin[j]), size_t(Lh.C) * pt::PN_TS * sizeof(u64)));
     }
@@ -752,8 +757,11 @@ int setup_panel(pt_pipeline* p) {
   return PT_OK;
 }
 
-// the weight buffer holding W^(t_next - 1) (before its pending update)
-int panel_cur(const pt_pipeline* p) { return p->learn ? int((p->t_next - 1) & 1) : 0; }
+// the weight buffer the next forward reads: W^(T) (backward-updated layers) or W^(T-1), whose
+// pending update the forward applies (T = t_next)
+int panel_cur(const pt_pipeline* p, const LayerHost& L) {
+  return !p->learn ? 0 : L.bw ? int(p->t_next & 1) : int((p->t_next - 1) & 1);
+}
 
 int panel_rowbuf(pt_pipeline* p, size_t floats) {
   if (p->rowbuf_floats >= floats && p->rowbuf) return PT_OK;
@@ -1387,7 +1395,8 @@ int pt_set_params(pt_pipeline* p, int32_t layer, const float* W, const float* b,
       const size_t nw = size_t(Lh->n_out) * Lh->n_in;
       PT_TRY(panel_rowbuf(p, nw));
       CUDA_TRY(cudaMemcpyAsync(p->rowbuf, W, nw * 4, k, p->stream));
-      pt::pn_to_tiles<<<592, 256, 0, p->stream>>>(p->rowbuf, Lh->Wt[panel_cur(p)], Lh->n_out, Lh->n_in, Lh->R, Lh->C);
+      pt::pn_to_tiles<<<592, 256, 0, p->stream>>>(p->rowbuf, Lh->Wt[panel_cur(p, *Lh)], Lh->n_out, Lh->n_in, Lh->R,
+                                                  Lh->C);
       CUDA_TRY(cudaGetLastError());
       Lh->set_tick = p->t_next;
     }
@@ -1417,7 +1426,7 @@ int pt_get_params(pt_pipeline* p, int32_t layer, float* W, float* b, int32_t whe
       // W^(T) = the stored W^(T-1) plus the update of tick T-1, if the next forward would apply it
       const long long T = p->t_next;
       const int h = stage_of_layer(p, layer);
-      const bool pend = p->learn && p->lr != 0.f && T - 1 >= 2LL * p->D - h - 1 && T - 1 >= Lh->set_tick;
+      const bool pend = p->learn && !Lh->bw && p->lr != 0.f && T - 1 >= 2LL * p->D - h - 1 && T - 1 >= Lh->set_tick;
       const float* sdel = nullptr;
       const float* ahat = nullptr;
       if (pend) {
@@ -1428,7 +1437,7 @@ int pt_get_params(pt_pipeline* p, int32_t layer, float* W, float* b, int32_t whe
       }
       const size_t nw = size_t(Lh->n_out) * Lh->n_in;
       PT_TRY(panel_rowbuf(p, nw));
-      pt::pn_from_tiles<<<592, 256, 0, p->stream>>>(Lh->Wt[panel_cur(p)], p->rowbuf, Lh->n_out, Lh->n_in, Lh->C, sdel,
+      pt::pn_from_tiles<<<592, 256, 0, p->stream>>>(Lh->Wt[panel_cur(p, *Lh)], p->rowbuf, Lh->n_out, Lh->n_in, Lh->C, sdel,
                                                     ahat, p->lr);
       CUDA_TRY(cudaGetLastError());
       CUDA_TRY(cudaMemcpyAsync(W, p->rowbuf, nw * 4, k, p->stream));

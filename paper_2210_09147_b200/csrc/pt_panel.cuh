@@ -61,6 +61,8 @@ struct PLayer {
   u64* gin[2];               // tagged delta of the previous layer = act' * g_in, [C*16] per tick parity
   float* dpl;                // plain copy of this layer's delta, [2][R*16] per tick parity (read at t+1)
   int n_in, n_out, R, C, act;
+  int bw;                    // learning, and the backward reads W: it applies the update and stores
+                             // W^(t+1) (buffer (t+1)&1); else the forward applies it (deferred)
   int cache_in, cache_out;   // word offsets of a_{l-1}, a_l in a stage cache slot
   long long set_tick;        // pt_set_params at this tick discarded the pending update of earlier ticks
 };
@@ -117,6 +119,11 @@ __device__ __forceinline__ bool pn_upd(const PParams& P, int h, long long t) {
 // the update of tick t-1 is still to be applied to layer L at tick t
 __device__ __forceinline__ bool pn_pending(const PParams& P, const PLayer& L, int h, long long t) {
   return pn_upd(P, h, t - 1) && t - 1 >= L.set_tick && !(P.dbg & 8);
+}
+// weight buffer the forward of tick t reads: W^(t) (backward-written layers), W^(t-1) (the
+// forward applies the pending update), or the only buffer (inference)
+__device__ __forceinline__ int pn_fbuf(const PParams& P, const PLayer& L, long long t) {
+  return !P.learn ? 0 : L.bw ? int(t & 1) : int((t - 1) & 1);
 }
 // the cache tick whose activations B(t) uses (act_delay reading)
 __device__ __forceinline__ long long pn_ct(const PParams& P, int h, long long t) {
@@ -397,9 +404,9 @@ __device__ void pn_producer(const PParams& P, const PLayer* layers, const PStage
     while (!pf.done && pf_idx < chunk + uint32_t(P.pf_chunks)) {
       const long long t = pf.t(P);
       if (pf.fwd()) {
-        prefetch_l2(pf.L->W[P.learn ? int((t - 1) & 1) : 0] + pf.foff(), uint32_t(pf.ntiles()) * PN_TILE * 4u);
+        prefetch_l2(pf.L->W[pn_fbuf(P, *pf.L, t)] + pf.foff(), uint32_t(pf.ntiles()) * PN_TILE * 4u);
       } else {
-        pn_tma_prefetch_3d(pf.L->tm[int((t - 1) & 1)], 0, pf.blk, pf.off);
+        pn_tma_prefetch_3d(pf.L->tm[int(t & 1)], 0, pf.blk, pf.off);
       }
       pf.advance(P, stages, layers);
       ++pf_idx;
@@ -411,7 +418,8 @@ __device__ void pn_producer(const PParams& P, const PLayer* layers, const PStage
     const int ti = cur.ti;
     const long long t = cur.t(P);
     if (P.learn && ti > 0) {
-      if (cur.fwd()) {
+      if (cur.fwd() && !cur.L->bw) {
+        // forward-written layer: my consumers stored my rows at tick ti-1; fenced yet?
         const int need = cur.fstep - nF + 1;  // the same layer's forward step of tick ti-1
         if (ld_acquire_cta_s32(fwd_fenced) < need) {
           const uint64_t t0 = globaltimer();
@@ -425,6 +433,7 @@ __device__ void pn_producer(const PParams& P, const PLayer* layers, const PStage
           }
         }
       } else if (ti > raw_ti) {
+        // backward-written weights: every CTA's tick ti-1 stores (fenced before its tick arrival)
         pn_wait_cnt(P.tick_end, u64(G) * u64(t), P);
         fence_proxy_async_global();
         raw_ti = ti;
@@ -447,12 +456,12 @@ __device__ void pn_producer(const PParams& P, const PLayer* layers, const PStage
       pn_jitter(P, 40);
       const uint32_t bytes = uint32_t(cur.ntiles()) * PN_TILE * 4u;
       mbar_arrive_expect_tx(&full[slot], bytes);
-      bulk_g2s(sdst, cur.L->W[P.learn ? int((t - 1) & 1) : 0] + cur.foff(), bytes, &full[slot], pol);
+      bulk_g2s(sdst, cur.L->W[pn_fbuf(P, *cur.L, t)] + cur.foff(), bytes, &full[slot], pol);
     } else {
       pn_trace(P, tr, P.trace_cap - P.trace_cap / 4, 41);
       pn_jitter(P, 41);
       mbar_arrive_expect_tx(&full[slot], uint32_t(PN_SLOT_FLOATS) * 4u);
-      pn_tma_load_3d(sdst, cur.L->tm[int((t - 1) & 1)], 0, cur.blk, cur.off, &full[slot], pol);
+      pn_tma_load_3d(sdst, cur.L->tm[int(t & 1)], 0, cur.blk, cur.off, &full[slot], pol);
     }
     ++chunk;
     cur.advance(P, stages, layers);
@@ -542,28 +551,35 @@ __device__ __forceinline__ void pn_fdot(const float* wb, const float* va, int nt
     for (int r = 0; r < 4; ++r) z[r] += dot4(w[q][r], a[q]);
 }
 
-// Backward chunk: acc += W^(t)[rows][own 4 columns] * delta[rows], W^(t) rebuilt from the
-// stored W^(t-1) with the pending update (the same fmaf as the forward).
-template <bool PEND, bool FULL>
-__device__ __forceinline__ void pn_bchunk(const float* wb, const float* dl, const float* sp, float4 ah4, int nt,
-                                          int tg, float4& acc) {
+// Backward chunk: acc += W^(t)[rows][own 4 columns] * delta[rows] (this thread: float4 f4 of
+// row tr of tiles tg, tg+4, ...), and W^(t+1) = W^(t) - lr delta[row] a_hat[col] stored to the
+// next buffer (UPD; the plain copy otherwise, during the warm-up)
+template <bool UPD, bool FULL>
+__device__ __forceinline__ void pn_bchunk(const float* wb, const float* dl, float nlr, float4 ah4, float* gdst,
+                                          int C, int nt, int tg, float4& acc) {
   float4 w[8];
-  float d[8], s[8];
+  float d[8];
 #pragma unroll
   for (int p = 0; p < 8; ++p) {
     const int tt = p * 4 + tg;
     const bool ok = FULL || tt < nt;
     w[p] = ok ? lds4(wb + tt * PN_TILE) : make_float4(0.f, 0.f, 0.f, 0.f);
     d[p] = ok ? dl[tt * PN_TS] : 0.f;
-    if (PEND) s[p] = ok ? sp[tt * PN_TS] : 0.f;
   }
 #pragma unroll
   for (int p = 0; p < 8; ++p) {
-    if (PEND) pn_fma4(w[p], s[p], ah4);
     acc.x = fmaf(w[p].x, d[p], acc.x);
     acc.y = fmaf(w[p].y, d[p], acc.y);
     acc.z = fmaf(w[p].z, d[p], acc.z);
     acc.w = fmaf(w[p].w, d[p], acc.w);
+  }
+#pragma unroll
+  for (int p = 0; p < 8; ++p) {
+    const int tt = p * 4 + tg;
+    if (FULL || tt < nt) {
+      if (UPD) pn_fma4(w[p], nlr * d[p], ah4);
+      __stcs(reinterpret_cast<float4*>(gdst + size_t(tt) * C * PN_TILE), w[p]);
+    }
   }
 }
 
@@ -740,7 +756,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constan
         const int nown = (RB.r1 - RB.r0) * PN_TS;
         const int nch = (L.C + PN_CT - 1) / PN_CT;  // chunks per row block
         const bool last = i == S.k - 1;
-        const bool pend = pn_pending(P, L, h, t);
+        const bool fw = P.learn && !L.bw;  // this forward applies the deferred update and stores W^(t)
+        const bool pend = fw && pn_pending(P, L, h, t);
         const long long Cp = pn_ct(P, h, t - 1);
         PN_TR(1);
         // every weight store of earlier forward steps is fenced for the producer's loads
@@ -769,7 +786,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constan
         // update-ahead: the pending update of the chunks the ring can hold, before the input
         // is there; W^(t) goes to the slot and to buffer t&1
         const int nck = nch * (RB.r1 - RB.r0);
-        const int ua = (P.learn && !(P.dbg & 2)) ? min(nck, P.nslot) : 0;
+        const int ua = (fw && !(P.dbg & 2)) ? min(nck, P.nslot) : 0;
         float* Wn = L.W[int(t & 1)];
         {
           int k = 0;
@@ -849,7 +866,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constan
             if (k >= ua) PN_TRC(7);
             float* wb = sm.ring + size_t(slot) * PN_SLOT_FLOATS + foff;
             const float* va = sm.va + c0 * PN_TS + f4 * 4;
-            if (k >= ua && P.learn) {
+            if (k >= ua && fw) {
               // beyond the update-ahead window: update (and store) here
               float* gd = Wn + (size_t(rb) * L.C + c0) * PN_TILE + foff;
               const float* vb = sm.vb + c0 * PN_TS + f4 * 4;
@@ -887,7 +904,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constan
             }
             const u64 w = pack_tv(a, tag_t);
             st_tv_gpu(Ccur + L.cache_out + row, w);
-            S.pcache[cmod4(t)][L.cache_out + row] = a;
             if (last && h < P.D) {
               if (rb == RB.r0) {
                 if (tid == 0) pn_wait_cnt(S.act_credit, u64(S.G_down) * u64(t), P);  // downstream read slot t&1 at t-1
@@ -951,23 +967,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constan
         const Rows RB{bk[0], bk[1]};
         const Rows CB{bk[2], bk[3]};
         const int ncol = (CB.r1 - CB.r0) * PN_TS;
-        const bool need_gin = !(h == 1 && i == 0);
-        const bool pend = pn_pending(P, L, h, t);
-        const long long Cp = pn_ct(P, h, t - 1);
+        const bool need_gin = !(h == 1 && i == 0);  // else: no weight read (and no update here: L.bw == 0)
         const bool stage_last = i == S.k - 1;
         const bool loss_src = stage_last && h == P.D;
         PN_TR(11);
-        // pending update of tick t-1 (plain copies from earlier ticks): own columns' a_hat and
-        // -lr * delta_{t-1} of every row
-        // (loads issued here, stored after the gather below: one round trip for everything)
-        const float* sap = (pend && need_gin) ? S.pcache[cmod4(Cp)] + L.cache_in + CB.r0 * PN_TS : nullptr;
-        const float* sdp = (pend && need_gin) ? L.dpl + size_t((t - 1) & 1) * nout : nullptr;
-        PPlain dpr;
-        float sa = 0.f;
-        if (sdp) {
-          dpr.issue(sdp, nout);
-          if (tid < ncol) sa = ldcg(sap + tid);
-        }
+        // a_hat_t of own columns (this layer's input at the cache tick): loads issued here,
+        // resolved after the gather
+        const u64* ahp = (need_gin && upd_now) ? Cc + L.cache_in + CB.r0 * PN_TS : nullptr;
+        const u64 ah = (ahp && tid < ncol) ? ld_tv_gpu(ahp + tid) : 0ull;
         // delta_l(t): the next layer's published vector, or (stage's last layer) the loss
         // gradient / the downstream stage's g_in times act'; delta_l(t-1) for the rebuild
         PV vg[2];
@@ -1001,11 +1008,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constan
             sm.va[j + e] = d;
           }
         });
-        if (sdp) {
-          dpr.store(sdp, nout, -P.lr, sm.vb);
-          if (tid < ncol) sm.sah[tid] = sa;
-          for (int j = tid + NCT; j < ncol; j += NCT) sm.sah[j] = ldcg(sap + j);
-        }
+        if (ahp) pn_small(ahp, ncol, ah, tag_of_tick(Ct), 1.f, sm.sah, P);
         cons_sync(NCT);
         if (stage_last && !loss_src && tid == 0) red_relaxed_sys(S.peer_g_credit, 1);  // gslot read
         if (loss_src && P.loss == 1) {
@@ -1038,7 +1041,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constan
         // the stage's last layer keeps its delta for the next tick (own forward rows); the bias step
         for (int j = RB.r0 * PN_TS + tid; j < RB.r1 * PN_TS; j += NCT) {
           const float d = sm.va[j];
-          if (stage_last) L.dpl[size_t(t & 1) * nout + j] = d;
+          if (stage_last && !L.bw) L.dpl[size_t(t & 1) * nout + j] = d;  // forward-applied update at t+1
           if (upd_now && j < L.n_out) {
             float* bp = sm.bias + sm.boff[S.first + i] + (j - RB.r0 * PN_TS);
             *bp = fmaf(nlr, d, *bp);
@@ -1056,21 +1059,22 @@ __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constan
               app = Cc + L.cache_in + cb * PN_TS + tid;
               ap = ld_tv_gpu(app);
             }
-            const float4 ah4 = pend ? lds4(sm.sah + (cb - CB.r0) * PN_TS + f4 * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+            const float4 ah4 = upd_now ? lds4(sm.sah + (cb - CB.r0) * PN_TS + f4 * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
             float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+            float* Wn = L.W[int((t + 1) & 1)] + size_t(cb) * PN_TILE + toff;  // W^(t+1), this column panel
             for (int j0 = 0; j0 < L.R; j0 += PN_CT) {
               const int nt = min(PN_CT, L.R - j0);
               const int slot = pn_take(sm, cslot, cphase, P);
               PN_TRC(8);
               const float* wb = sm.ring + size_t(slot) * PN_SLOT_FLOATS + toff;
               const float* dl = sm.va + j0 * PN_TS + tr;
-              const float* sp = sm.vb + j0 * PN_TS + tr;
-              if (pend) {
-                if (nt == PN_CT) pn_bchunk<true, true>(wb, dl, sp, ah4, nt, tg, acc);
-                else pn_bchunk<true, false>(wb, dl, sp, ah4, nt, tg, acc);
+              float* gd = Wn + size_t(j0) * L.C * PN_TILE;
+              if (upd_now) {
+                if (nt == PN_CT) pn_bchunk<true, true>(wb, dl, nlr, ah4, gd, L.C, nt, tg, acc);
+                else pn_bchunk<true, false>(wb, dl, nlr, ah4, gd, L.C, nt, tg, acc);
               } else {
-                if (nt == PN_CT) pn_bchunk<false, true>(wb, dl, sp, ah4, nt, tg, acc);
-                else pn_bchunk<false, false>(wb, dl, sp, ah4, nt, tg, acc);
+                if (nt == PN_CT) pn_bchunk<false, true>(wb, dl, nlr, ah4, gd, L.C, nt, tg, acc);
+                else pn_bchunk<false, false>(wb, dl, nlr, ah4, gd, L.C, nt, tg, acc);
               }
               __syncwarp();
               if (lane == 0) mbar_arrive(&sm.empty[slot]);
@@ -1107,7 +1111,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constan
                 const float av = pn_resolve(app, ap, tag_of_tick(Ct), false, P);
                 const float d = o * dact_fn(Lp->act, av);
                 st_tv_gpu(L.gin[t & 1] + col, pack_tv(d, tag_t));
-                Lp->dpl[size_t(t & 1) * (Lp->R * PN_TS) + col] = d;  // for tick t+1
+                if (!Lp->bw) Lp->dpl[size_t(t & 1) * (Lp->R * PN_TS) + col] = d;  // forward-applied update at t+1
               }
             }
           }
