@@ -234,8 +234,7 @@ def extra_configs(peak):
                 best = min(best, p.last_kernel_ms())
             us = best * 1e3 / ticks
             byt = algorithmic_bytes_per_tick(widths, learn)
-            res[name] = {"workload": desc, "kernel": "pt::tile_kernel (tcgen05)" if p.kernel_path == "tile"
-                         else "pt::tick_kernel", "tick_us": round(us, 1), "samples_per_s": round(M * 1e6 / us, 1),
+            res[name] = {"workload": desc, "kernel": KERNEL_NAMES[p.kernel_path], "tick_us": round(us, 1), "samples_per_s": round(M * 1e6 / us, 1),
                          "achieved_gbs": round(byt / (us * 1e-6) / 1e9, 1),
                          "frac_of_hbm_roofline": round(byt / (us * 1e-6) / 1e9 / peak, 4)}
             p.close()
@@ -246,9 +245,12 @@ def extra_configs(peak):
     return res
 
 
-def load_traffic():
-    """dram bytes per tick of the tick kernel from the committed ncu capture, if any."""
-    path = os.path.join(ROOT, "profiles", "ncu_tick_kernel.json")
+KERNEL_NAMES = {"panel": "pt::panel_kernel", "tile": "pt::tile_kernel (tcgen05)", "tick": "pt::tick_kernel"}
+
+
+def load_traffic(path_kind="panel"):
+    """dram bytes per tick of the bench kernel from the committed ncu capture, if any."""
+    path = os.path.join(ROOT, "profiles", f"ncu_{path_kind}_kernel.json")
     try:
         with open(path) as f:
             d = json.load(f)
@@ -337,6 +339,7 @@ def main():
     pipe.run(xs, ys, T)
     pipe.sync()
     launch_ms = pipe.last_kernel_ms()
+    launch_ms_local = launch_ms
     total_ms = sum(step_ms)
     if world > 1:
         t = torch.tensor([total_ms, launch_ms], dtype=torch.float64)
@@ -378,6 +381,22 @@ def main():
         el = time.perf_counter() - t0
         step_api = {"value": round(n_calls / el, 2), "unit": "samples/s", "us_per_call": round(el / n_calls * 1e6, 2),
                     "api": "engine.Pipeline.step -> pt_step (host buffers, one synchronous tick per call)"}
+    # per-rank (per-stage) roofline: each rank's own launch time over its own stage's bytes
+    peak_r = None
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peak_r = float(json.load(f)["hbm_gbs"])
+    except Exception:
+        peak_r = 6650.0
+    mine = {"rank": rank, "stages": [pipe.local_first + 1, pipe.local_first + pipe.local_count],
+            "kernel": KERNEL_NAMES[pipe.kernel_path], "launch_ms": round(launch_ms_local, 4),
+            "algorithmic_bytes_per_launch": bytes_tick * T,
+            "achieved_gbs": round(bytes_tick * T / (launch_ms_local / 1e3) / 1e9, 1),
+            "frac": round(bytes_tick * T / (launch_ms_local / 1e3) / 1e9 / peak_r, 4)}
+    per_rank = [mine]
+    if world > 1:
+        per_rank = [None] * world
+        dist.all_gather_object(per_rank, mine, group=gloo)
     h2d = T * BATCH * (widths[0] + widths[-1]) * 4
     d2h = T * BATCH * widths[-1] * 4 + T * 4 + T
 
@@ -392,12 +411,13 @@ def main():
             peak, peak_src = float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
         peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
-    tpt, ncu = load_traffic()
+    kpath = pipe.kernel_path
+    tpt, ncu = load_traffic(kpath)
     if ncu is None or ncu.get("config") != {"width": args.width, "layers": args.layers, "stages": D}:
         tpt = None  # the committed capture is for another workload
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "traffic": (tpt * T if tpt else None),
-            "kernel": "pt::tick_kernel", "algorithmic_bytes_per_launch": bytes_tick * T,
+            "kernel": KERNEL_NAMES[kpath], "algorithmic_bytes_per_launch": bytes_tick * T,
             "launch_ms": round(launch_ms, 4), "peak_source": peak_src}
     cpu = None
     if not args.no_cpu_baseline and world == 1:
@@ -419,6 +439,7 @@ def main():
         "latency": {"tick_us": round(1e3 * total_ms / (args.steps * T), 2),
                     "sample_latency_ticks": D, "sample_latency_us": round(1e3 * total_ms / (args.steps * T) * D, 2)},
         "roofline": roof,
+        "per_rank": per_rank,
         "cpu_baseline": cpu,
         # job-wide bytes: xs enter at stage 1's GPU, targets and results at stage D's
         "e2e": {"value": round(e2e_value, 2), "unit": "samples/s", "h2d_bytes_per_step": h2d,

@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define PT_ABI_VERSION 1
+#define PT_ABI_VERSION 2
 
 /* error codes */
 #define PT_OK            0
@@ -83,6 +83,14 @@ typedef struct pt_config {
   int32_t local_stage_count;         /*   device; count 0 = all stages (single process) */
   int32_t grid;                      /* CTAs per device; 0 = one per SM */
   int32_t timeout_ms;                /* device watchdog for cross-stage waits; 0 = 30000 */
+  const int32_t* device_of_stage;    /* D CUDA device ordinals ("the list of available
+                                        GPU devices ... it can be smaller, making multiple stages
+                                        execute on the same device"), or NULL = the current device.
+                                        Stages of one device must be contiguous. When the local
+                                        stages span several devices the handle drives one part per
+                                        device from this process: peer access is enabled and the
+                                        parts exchange activations / gradients by peer stores over
+                                        NVLink (same tagged-slot + credit protocol as CUDA IPC) */
 } pt_config;
 
 /* pipeline_build: allocate all buffers, zero slots/caches, init nothing
@@ -124,6 +132,11 @@ int pt_get_stream(const pt_pipeline* p, void** stream);
 /* Device time (ms) of the tick kernel of the last pt_run/pt_step, from CUDA events on the
  * handle's stream; valid after pt_sync. */
 int pt_last_kernel_ms(pt_pipeline* p, float* ms);
+
+/* Device ordinal that runs 1-based `stage` (device_of_stage, or the creating device); -1 if
+ * the stage is not local. Device-buffer callers of a multi-device handle pass xs on stage 1's
+ * device and ys / outs / losses / valid on stage D's. */
+int32_t pt_stage_device(const pt_pipeline* p, int32_t stage);
 
 /* Next global tick index (number of ticks executed so far). */
 int64_t pt_tick(pt_pipeline* p);

@@ -33,7 +33,7 @@ PT_OPT = {"sgd": 0, "adam": 1}
 EXPORTS = (
     "pt_create", "pt_set_params", "pt_get_params", "pt_step", "pt_run", "pt_sync",
     "pt_set_stream", "pt_get_stream", "pt_last_kernel_ms", "pt_tick", "pt_set_trace", "pt_get_trace",
-    "pt_ipc_export", "pt_ipc_import", "pt_kernel_path",
+    "pt_ipc_export", "pt_ipc_import", "pt_kernel_path", "pt_stage_device",
     "pt_destroy", "pt_last_error", "pt_abi_version",
 )
 
@@ -55,6 +55,7 @@ class PTConfig(ctypes.Structure):
         ("local_stage_count", ctypes.c_int32),
         ("grid", ctypes.c_int32),
         ("timeout_ms", ctypes.c_int32),
+        ("device_of_stage", ctypes.POINTER(ctypes.c_int32)),
     ]
 
 
@@ -103,6 +104,8 @@ def load():
     lib.pt_tick.restype = ctypes.c_int64
     lib.pt_kernel_path.argtypes = [P]
     lib.pt_kernel_path.restype = ctypes.c_int32
+    lib.pt_stage_device.argtypes = [P, ctypes.c_int32]
+    lib.pt_stage_device.restype = ctypes.c_int32
     lib.pt_ipc_export.argtypes = [P, ctypes.c_int32, P, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]
     lib.pt_ipc_import.argtypes = [P, P, ctypes.c_size_t]
     lib.pt_set_trace.argtypes = [P, ctypes.c_int32, ctypes.c_int32]

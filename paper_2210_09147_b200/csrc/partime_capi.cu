@@ -11,6 +11,7 @@
 #include <unistd.h>
 
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -235,6 +236,37 @@ struct pt_pipeline {
   pt::TStage* d_tstages = nullptr;
   std::vector<pt::TLayer> t_layers_host;
   int policy = 0;                                     // weight-load L2 hint (env PT_POLICY)
+  // host outputs of a PT_HOST run enqueued without waiting (multi-device handles launch every
+  // part before waiting for any): copied out of the pinned staging area at finish_impl
+  struct Pending {
+    bool active = false;
+    int64_t n = 0;
+    float *outs = nullptr, *losses = nullptr, *pin_o = nullptr, *pin_l = nullptr;
+    uint8_t *valid = nullptr, *pin_v = nullptr;
+    size_t st_o = 0, st_l = 0, st_v = 0;
+  } pend;
+  // multi-device handle (pt_config.device_of_stage): one part per run of stages on one device,
+  // each a complete single-device handle; the parts' neighbour stages exchange through peer
+  // memory. Empty for a single-device handle.
+  std::vector<pt_pipeline*> parts;
+  bool group() const { return !parts.empty(); }
+  // resident pt_step (pt_panel.cuh PParams::resident): one mapped host block holding the
+  // completion record, the request words and the x / target / output rings
+  struct Resident {
+    bool on = false;
+    long long t_start = 0;
+    int ring = 0, ldx = 0, fy = 0;
+    size_t bytes = 0;
+    void* host = nullptr;
+    ptrdiff_t dev_off = 0;  // device alias of the mapped block minus its host address
+    pt::PResDone* done = nullptr;
+    long long* req = nullptr;
+    int* flag = nullptr;
+    float *x = nullptr, *y = nullptr, *out = nullptr;
+    u64* xin = nullptr;
+    long long* relay = nullptr;
+    float* lpart = nullptr;
+  } res;
 
   bool has_first() const { return local_first == 0; }
   bool has_last() const { return local_first + local_count == D; }
@@ -258,6 +290,20 @@ struct BusyGuard {
   }
   ~BusyGuard() {
     if (ok) p->busy.store(0);
+  }
+};
+
+// Every entry point runs on the handle's device, whatever the caller's current device is
+// (a multi-device handle drives several devices from one thread).
+struct DevGuard {
+  int old = -1;
+  explicit DevGuard(int dev) {
+    if (cudaGetDevice(&old) != cudaSuccess) old = -1;
+    if (old != dev) cudaSetDevice(dev);
+  }
+  ~DevGuard() {
+    int cur = -1;
+    if (old >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != old) cudaSetDevice(old);
   }
 };
 
@@ -294,6 +340,7 @@ int ensure(pt_pipeline* p, T** buf, size_t* cap, size_t need, size_t elems_per) 
 }
 
 int upload_panel_desc(pt_pipeline* p);
+int group_finish(pt_pipeline* p);
 
 int upload_desc(pt_pipeline* p) {
   std::vector<pt::LayerDev> ld(p->layers.size());
@@ -726,7 +773,7 @@ int setup_panel(pt_pipeline* p) {
                         p->layers.size() * 7 * sizeof(int));  // + bias offsets and block ranges
   const int bias = a128(bias_rows * 4);
   const int tail = 2 * a128(size_t(maxw) * 4) + a128(size_t(maxrown) * 4) + a128(size_t(maxcoln) * 4) +
-                   a128((256 + 64) * 4) + a128(3 * pt::PN_MAXSLOT * 8) + desc + bias;
+                   a128((256 + 64 + 32) * 4) + a128(3 * pt::PN_MAXSLOT * 8) + desc + bias;
   const int slot_bytes = pt::PN_SLOT_FLOATS * 4;
   int nslot = std::min(pt::PN_MAXSLOT, (pt::SMEM_MAX - tail) / slot_bytes);
   if (const char* e = getenv("PT_NSLOT")) nslot = std::min(nslot, std::max(2, atoi(e)));
@@ -743,7 +790,7 @@ int setup_panel(pt_pipeline* p) {
   p->pn_sah = off;
   off += a128(size_t(maxcoln) * 4);
   p->pn_red = off;
-  off += a128((256 + 64) * 4);
+  off += a128((256 + 64 + 32) * 4);  // red[256], scal[64], flags[32] (PSmem)
   p->pn_bar = off;
   off += a128(3 * pt::PN_MAXSLOT * 8);
   p->pn_desc = off;
@@ -1048,9 +1095,212 @@ int read_status(pt_pipeline* p) {
   return PT_OK;
 }
 
-int run_impl(pt_pipeline* p, const float* xs, const float* ys, int64_t n, float* outs, float* losses,
-             uint8_t* valid, int where) {
+// Wait for the handle's stream, copy pending host outputs out of the pinned staging area and
+// report deferred device-side errors.
+int finish_impl(pt_pipeline* p) {
+  CUDA_TRY(cudaStreamSynchronize(p->stream));
+  if (p->pend.active) {
+    pt_pipeline::Pending& q = p->pend;
+    if (q.st_o) memcpy(q.outs, q.pin_o, q.st_o * 4);
+    if (q.st_l) memcpy(q.losses, q.pin_l, q.st_l * 4);
+    if (q.st_v) memcpy(q.valid, q.pin_v, size_t(q.n));
+    q.active = false;
+  }
+  return read_status(p);
+}
+
+// Launch parameters of the panel kernel shared by pt_run and the resident pt_step.
+void panel_common(pt_pipeline* p, pt::PParams& Q) {
+  memset(&Q, 0, sizeof(Q));
+  Q.stages = p->d_pstages;
+  Q.layers = p->d_players;
+  Q.n_stages = int(p->stages.size());
+  Q.n_layers = int(p->layers.size());
+  Q.D = p->D;
+  Q.learn = p->learn;
+  Q.act_delay = p->act_delay;
+  Q.G = p->G;
+  Q.F = p->F();
+  Q.loss = p->loss;
+  Q.lr = p->lr;
+  Q.ldx = p->stage_ld0(0);
+  Q.yhist = p->yhist;
+  Q.yh = p->yh;
+  Q.tick_end = p->d_tick_end;
+  Q.status = p->d_status;
+  Q.bad_target = p->d_bad_target;
+  Q.timeout_ns = p->timeout_ns;
+  Q.nslot = p->pn_nslot;
+  Q.va_off = p->pn_va;
+  Q.vb_off = p->pn_vb;
+  Q.sown_off = p->pn_sown;
+  Q.sah_off = p->pn_sah;
+  Q.red_off = p->pn_red;
+  Q.bar_off = p->pn_bar;
+  Q.desc_off = p->pn_desc;
+  Q.bias_off = p->pn_bias;
+  Q.pf_chunks = p->pn_pf;
+  Q.psleep = getenv("PT_PSLEEP") ? atoi(getenv("PT_PSLEEP")) : 0;
+  Q.dbg = getenv("PT_PN_DBG") ? atoi(getenv("PT_PN_DBG")) : 0;
+  Q.policy = p->policy;
+  Q.trace = p->d_trace;
+  Q.trace_cap = p->trace_cap;
+  Q.trace_cta = p->trace_cta;
+  Q.jitter_mask = 3;
+}
+
+// ---------------------------------------------------------------- resident pt_step
+// The per-sample drop-in (pipeline_step; Pipeline.forward)
+// without a launch per sample: PAPER.md:600-605 removed the per-tick enqueue cost with CUDA
+// Graphs; here one persistent panel-kernel launch serves consecutive pt_step calls (see
+// PParams::resident in pt_panel.cuh). Any other entry point stops it first (resident_stop).
+bool resident_eligible(const pt_pipeline* p) {
+  if (!p->panel || p->group() || !p->has_first() || !p->has_last() || p->M != 1) return false;
+  const char* e = getenv("PT_RESIDENT");
+  return !(e && atoi(e) == 0);
+}
+
+int resident_alloc(pt_pipeline* p) {
+  pt_pipeline::Resident& r = p->res;
+  if (r.host) return PT_OK;
+  r.ring = p->D + 2;
+  r.ldx = p->stage_ld0(0);
+  r.fy = p->Fy();
+  const size_t nx = size_t(r.ring) * r.ldx, ny = size_t(r.ring) * r.fy, no = size_t(2) * p->F();
+  r.bytes = align_up(sizeof(pt::PResDone), 64) + 64 + (nx + ny + no) * 4;
+  CUDA_TRY(cudaHostAlloc(&r.host, r.bytes, cudaHostAllocMapped));
+  memset(r.host, 0, r.bytes);
+  char* h = static_cast<char*>(r.host);
+  r.done = reinterpret_cast<pt::PResDone*>(h);
+  h += align_up(sizeof(pt::PResDone), 64);
+  r.req = reinterpret_cast<long long*>(h);
+  r.flag = reinterpret_cast<int*>(h + 8);
+  h += 64;
+  r.x = reinterpret_cast<float*>(h);
+  r.y = r.x + nx;
+  r.out = r.y + ny;
+  void* dh = nullptr;
+  CUDA_TRY(cudaHostGetDevicePointer(&dh, r.host, 0));
+  r.dev_off = static_cast<char*>(dh) - static_cast<char*>(r.host);
+  PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&r.xin), size_t(2) * r.ldx * sizeof(u64)));
+  PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&r.relay), 64));
+  PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&r.lpart), size_t(2) * p->G * sizeof(float)));
+  return PT_OK;
+}
+
+template <class T>
+T* to_dev(const pt_pipeline* p, T* hptr) {
+  return reinterpret_cast<T*>(reinterpret_cast<char*>(hptr) + p->res.dev_off);
+}
+
+int resident_start(pt_pipeline* p) {
   PT_TRY(check_ready(p));
+  PT_TRY(resident_alloc(p));
+  if (p->legacy_dirty) {
+    CUDA_TRY(cudaStreamSynchronize(0));
+    p->legacy_dirty = false;
+  }
+  pt_pipeline::Resident& r = p->res;
+  *reinterpret_cast<volatile long long*>(r.req) = p->t_next;  // nothing requested yet
+  *reinterpret_cast<volatile long long*>(&r.done->tick) = -1;
+  CUDA_TRY(cudaMemsetAsync(r.relay, 0, 64, p->stream));
+  pt::PParams Q;
+  panel_common(p, Q);
+  Q.t0 = p->t_next;
+  Q.n = std::numeric_limits<int>::max();
+  Q.loss_part = r.lpart;
+  Q.resident = 1;
+  Q.hreq = to_dev(p, r.req);
+  Q.hflag = to_dev(p, r.flag);
+  Q.relay = r.relay;
+  Q.rx = to_dev(p, r.x);
+  Q.ry = to_dev(p, r.y);
+  Q.rring = r.ring;
+  Q.xin = r.xin;
+  Q.rout = to_dev(p, r.out);
+  Q.rdone = to_dev(p, r.done);
+  if (p->d_trace) CUDA_TRY(cudaMemsetAsync(p->d_trace, 0, size_t(p->trace_cap) * sizeof(u64), p->stream));
+  void* qargs[] = {&Q};
+  CUDA_TRY(cudaLaunchCooperativeKernel((const void*)pt::panel_kernel<0>, dim3(p->G), dim3(pt::NTHREADS), qargs,
+                                       size_t(p->pn_smem), p->stream));
+  r.on = true;
+  r.t_start = p->t_next;
+  return PT_OK;
+}
+
+// Post a stop, wait for the launch to drain, and queue the last D-1 posted targets for the next
+// pt_run (target queue).
+int resident_stop(pt_pipeline* p) {
+  pt_pipeline::Resident& r = p->res;
+  if (!r.on) return PT_OK;
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  *reinterpret_cast<volatile long long*>(r.req) = pt::PN_STOP;
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  r.on = false;
+  CUDA_TRY(cudaStreamSynchronize(p->stream));
+  const int Fy = p->Fy();
+  for (long long s = std::max(r.t_start, p->t_next - (p->D - 1)); s < p->t_next; ++s)
+    CUDA_TRY(cudaMemcpyAsync(p->yhist + size_t(s % p->yh) * Fy, r.y + size_t(s % r.ring) * Fy, size_t(Fy) * 4,
+                             cudaMemcpyHostToDevice, p->stream));
+  CUDA_TRY(cudaStreamSynchronize(p->stream));
+  return read_status(p);
+}
+
+// One tick through the resident launch: write x_t and gamma_t into the mapped rings, post the
+// request, wait for the completion record.
+int resident_step(pt_pipeline* p, const float* x, const float* y, float* out, float* loss, int32_t* valid) {
+  if (!x) return fail(PT_EINVAL, "x is required on the process that owns stage 1");
+  if (p->learn && !y) return fail(PT_EINVAL, "targets are required for online learning (stage D)");
+  if (!p->res.on) PT_TRY(resident_start(p));
+  pt_pipeline::Resident& r = p->res;
+  const long long t = p->t_next;
+  const int n0 = p->dims[0], Fy = p->Fy(), F = p->F();
+  memcpy(r.x + size_t(t % r.ring) * r.ldx, x, size_t(n0) * 4);
+  if (y) memcpy(r.y + size_t(t % r.ring) * Fy, y, size_t(Fy) * 4);
+  else memset(r.y + size_t(t % r.ring) * Fy, 0, size_t(Fy) * 4);
+  *reinterpret_cast<volatile int*>(r.flag) = y ? 1 : 0;
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  *reinterpret_cast<volatile long long*>(r.req) = t + 1;
+  volatile long long* dt = &r.done->tick;
+  const auto t_begin = std::chrono::steady_clock::now();
+  unsigned spins = 0;
+  while (*dt != t + 1) {
+    if ((++spins & 0xFFFu) == 0) {
+      const cudaError_t q = cudaStreamQuery(p->stream);
+      if (q != cudaErrorNotReady) {  // the launch ended without completing the step
+        r.on = false;
+        if (q != cudaSuccess) return fail(PT_ECUDA, std::string("resident launch failed: ") + cudaGetErrorString(q));
+        PT_TRY(read_status(p));
+        return fail(PT_ESTATE, "resident launch ended before completing step " + std::to_string(t));
+      }
+      if (std::chrono::steady_clock::now() - t_begin > std::chrono::nanoseconds(4 * p->timeout_ns)) {
+        p->broken = true;
+        return fail(PT_ETIMEOUT, "resident step " + std::to_string(t) + " did not complete");
+      }
+    }
+  }
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  p->t_next = t + 1;
+  const pt::PResDone d = *const_cast<const pt::PResDone*>(r.done);
+  if (out) memcpy(out, r.out + size_t(t & 1) * F, size_t(F) * 4);
+  if (loss) *loss = d.loss;
+  if (valid) *valid = d.valid;
+  if (d.status != pt::ST_OK) {
+    PT_TRY(resident_stop(p));
+    return fail(PT_ETIMEOUT, "a stage waited longer than timeout_ms; pipeline state is lost");
+  }
+  if (d.bad_target != std::numeric_limits<long long>::max()) {
+    PT_TRY(resident_stop(p));  // read_status reports and clears the device flag
+    return PT_EINVAL;
+  }
+  if (d.bad_loss >= 0) return fail(PT_ENONFINITE, "non-finite loss at step " + std::to_string(d.bad_loss));
+  return PT_OK;
+}
+
+int run_impl(pt_pipeline* p, const float* xs, const float* ys, int64_t n, float* outs, float* losses,
+             uint8_t* valid, int where, bool wait = true) {
+  PT_TRY(check_ready(p));
+  if (p->pend.active) return fail(PT_EBUSY, "contract violation: previous run not finished (pt_sync)");
   if (n <= 0) return PT_OK;
   if (p->legacy_dirty) {
     CUDA_TRY(cudaStreamSynchronize(0));
@@ -1204,47 +1454,14 @@ int run_impl(pt_pipeline* p, const float* xs, const float* ys, int64_t n, float*
 
   if (p->panel) {
     pt::PParams Q;
-    memset(&Q, 0, sizeof(Q));
-    Q.stages = p->d_pstages;
-    Q.layers = p->d_players;
-    Q.n_stages = int(p->stages.size());
-    Q.n_layers = int(p->layers.size());
-    Q.D = p->D;
-    Q.learn = p->learn;
-    Q.act_delay = p->act_delay;
-    Q.G = p->G;
-    Q.F = F;
-    Q.loss = p->loss;
-    Q.lr = p->lr;
+    panel_common(p, Q);
     Q.xs = first ? p->xs_pad : nullptr;
     Q.ldx = ld0;
     Q.ys = ys_dev;
-    Q.yhist = p->yhist;
-    Q.yh = p->yh;
     Q.outs = outs_dev;
     Q.loss_part = last ? p->loss_part : nullptr;
     Q.t0 = p->t_next;
     Q.n = int(n);
-    Q.tick_end = p->d_tick_end;
-    Q.status = p->d_status;
-    Q.bad_target = p->d_bad_target;
-    Q.timeout_ns = p->timeout_ns;
-    Q.nslot = p->pn_nslot;
-    Q.va_off = p->pn_va;
-    Q.vb_off = p->pn_vb;
-    Q.sown_off = p->pn_sown;
-    Q.sah_off = p->pn_sah;
-    Q.red_off = p->pn_red;
-    Q.bar_off = p->pn_bar;
-    Q.desc_off = p->pn_desc;
-    Q.bias_off = p->pn_bias;
-    Q.pf_chunks = p->pn_pf;
-    Q.psleep = getenv("PT_PSLEEP") ? atoi(getenv("PT_PSLEEP")) : 0;
-    Q.dbg = getenv("PT_PN_DBG") ? atoi(getenv("PT_PN_DBG")) : 0;
-    Q.policy = p->policy;
-    Q.trace = p->d_trace;
-    Q.trace_cap = p->trace_cap;
-    Q.trace_cta = p->trace_cta;
     Q.jitter = P.jitter;
     Q.jitter_mask = P.jitter_mask;
     void* qargs[] = {&Q};
@@ -1332,15 +1549,174 @@ int run_impl(pt_pipeline* p, const float* xs, const float* ys, int64_t n, float*
   }
   p->t_next += n;
   if (where == PT_HOST) {
-    CUDA_TRY(cudaStreamSynchronize(p->stream));
     if (staged && last) {
-      if (st_o) memcpy(outs, pin_o, st_o * 4);
-      if (st_l) memcpy(losses, pin_l, st_l * 4);
-      if (st_v) memcpy(valid, pin_v, size_t(n));
+      p->pend.n = n;
+      p->pend.outs = outs;
+      p->pend.losses = losses;
+      p->pend.valid = valid;
+      p->pend.pin_o = pin_o;
+      p->pend.pin_l = pin_l;
+      p->pend.pin_v = pin_v;
+      p->pend.st_o = st_o;
+      p->pend.st_l = st_l;
+      p->pend.st_v = st_v;
+      p->pend.active = true;
     }
-    return read_status(p);
+    if (!wait) return PT_OK;
+    return finish_impl(p);
   }
   return PT_OK;
+}
+
+
+// ---------------------------------------------------------------- multi-device handles
+// pt_config.device_of_stage spreads the local stages over several devices of this process
+// (SURVEY.md §8(b)). Each maximal run of stages on one device becomes a part:
+// a complete single-device handle with local_stage_first/count = that run. Neighbouring parts
+// import each other's comm blocks by device pointer (peer access enabled), so the kernels
+// store activations, gradients and credits straight into the neighbour's memory with
+// system-scope stores, exactly as across processes with CUDA IPC.
+//
+// PT_VIRTUAL_DEVICES=1 (testing on a one-GPU box): device ordinals are taken modulo the device
+// count, and parts that land on one physical device split its SMs (grid = SMs / parts there),
+// so their cooperative launches are co-resident.
+
+pt_pipeline* part_of_layer(pt_pipeline* p, int layer) {
+  for (pt_pipeline* q : p->parts)
+    if (layer >= q->layer_base && layer < q->layer_base + int(q->layers.size())) return q;
+  return nullptr;
+}
+
+int connect_parts(pt_pipeline* a, pt_pipeline* b) {
+  // a owns stages [.., s], b owns [s+1, ..] (1-based s = a->local_first + a->local_count)
+  const int s = a->local_first + a->local_count;
+  char blob[256];
+  size_t len = 0;
+  if (a->device != b->device) {
+    int ab = 0, ba = 0;
+    CUDA_TRY(cudaDeviceCanAccessPeer(&ab, a->device, b->device));
+    CUDA_TRY(cudaDeviceCanAccessPeer(&ba, b->device, a->device));
+    if (!ab || !ba)
+      return fail(PT_EUNSUPPORTED, "devices " + std::to_string(a->device) + " and " + std::to_string(b->device) +
+                                       " have no peer access (one process per GPU: dist.build_distributed)");
+    for (int k = 0; k < 2; ++k) {
+      DevGuard dg(k ? b->device : a->device);
+      cudaError_t e = cudaDeviceEnablePeerAccess(k ? a->device : b->device, 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled) {
+        cudaGetLastError();
+      } else if (e != cudaSuccess) {
+        return fail(PT_ECUDA, std::string("cudaDeviceEnablePeerAccess: ") + cudaGetErrorString(e));
+      }
+    }
+  }
+  PT_TRY(pt_ipc_export(a, s, blob, sizeof(blob), &len));
+  PT_TRY(pt_ipc_import(b, blob, len));
+  PT_TRY(pt_ipc_export(b, s + 1, blob, sizeof(blob), &len));
+  PT_TRY(pt_ipc_import(a, blob, len));
+  return PT_OK;
+}
+
+int create_group(const pt_config* c, pt_pipeline* p) {
+  std::string why;
+  if (validate(c, &why) != PT_OK) return fail(PT_EINVAL, why);
+  const int D = c->n_stages;
+  int ndev = 0;
+  CUDA_TRY(cudaGetDeviceCount(&ndev));
+  const char* ve = getenv("PT_VIRTUAL_DEVICES");
+  const bool virt = ve && atoi(ve) != 0;
+  std::vector<int> dev(D);
+  for (int h = 0; h < D; ++h) {
+    const int d = c->device_of_stage[h];
+    if (d < 0 || (!virt && d >= ndev))
+      return fail(PT_EINVAL, "device_of_stage[" + std::to_string(h) + "] = " + std::to_string(d) +
+                                 " is not a device of this process (" + std::to_string(ndev) + " visible)");
+    dev[h] = d;
+  }
+  for (int h = 1; h < D; ++h)
+    for (int g = 0; g + 1 < h; ++g)
+      if (dev[g] == dev[h] && dev[h - 1] != dev[h])
+        return fail(PT_EINVAL, "stages of one device must be contiguous (device " + std::to_string(dev[h]) +
+                                   " holds stages " + std::to_string(g + 1) + " and " + std::to_string(h + 1) + ")");
+  const int lo = c->local_stage_count ? c->local_stage_first : 0;
+  const int hi = c->local_stage_count ? lo + c->local_stage_count : D;
+  std::vector<std::pair<int, int>> runs;  // (first stage, count), 0-based
+  for (int h = lo; h < hi; ++h) {
+    if (runs.empty() || dev[h] != dev[runs.back().first]) runs.push_back({h, 0});
+    ++runs.back().second;
+  }
+  std::vector<int> phys(runs.size());
+  std::vector<int> share(std::max(ndev, 1), 0);
+  for (size_t i = 0; i < runs.size(); ++i) {
+    phys[i] = dev[runs[i].first] % std::max(ndev, 1);
+    ++share[phys[i]];
+  }
+  p->L = c->n_layers;
+  p->D = D;
+  p->M = c->batch;
+  p->loss = c->loss;
+  p->learn = c->learn ? 1 : 0;
+  p->dims.assign(c->dims, c->dims + p->L + 1);
+  p->sfl.assign(c->stage_first_layer, c->stage_first_layer + D + 1);
+  p->local_first = lo;
+  p->local_count = hi - lo;
+  p->device = phys[0];
+  for (size_t i = 0; i < runs.size(); ++i) {
+    pt_config sub = *c;
+    sub.device_of_stage = nullptr;
+    sub.local_stage_first = runs[i].first;
+    sub.local_stage_count = runs[i].second;
+    if (sub.grid == 0 && share[phys[i]] > 1) {
+      int sms = 0;
+      CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, phys[i]));
+      sub.grid = sms / share[phys[i]];
+    }
+    DevGuard dg(phys[i]);
+    pt_pipeline* q = nullptr;
+    PT_TRY(pt_create(&sub, &q));
+    p->parts.push_back(q);
+  }
+  for (size_t i = 0; i + 1 < p->parts.size(); ++i) PT_TRY(connect_parts(p->parts[i], p->parts[i + 1]));
+  return PT_OK;
+}
+
+// Enqueue n ticks on every part (stage-1 part first; none waits), then, for host buffers,
+// wait for all of them. Inputs go to the part that owns stage 1, targets and outputs to the
+// part that owns stage D.
+int group_run(pt_pipeline* p, const float* xs, const float* ys, int64_t n, float* outs, float* losses,
+              uint8_t* valid, int where) {
+  if (n <= 0) return PT_OK;
+  if (p->has_first() && !xs) return fail(PT_EINVAL, "xs is required on the process that owns stage 1");
+  if (p->has_last() && p->learn && !ys) return fail(PT_EINVAL, "targets are required for online learning (stage D)");
+  for (pt_pipeline* q : p->parts) PT_TRY(check_ready(q));
+  for (pt_pipeline* q : p->parts) {
+    DevGuard dg(q->device);
+    const bool f = q->has_first(), l = q->has_last();
+    const int r = run_impl(q, f ? xs : nullptr, l ? ys : nullptr, n, l ? outs : nullptr, l ? losses : nullptr,
+                           l ? valid : nullptr, where, false);
+    if (r != PT_OK) {
+      // the parts already launched wait for this one until their watchdog fires (timeout_ms)
+      for (pt_pipeline* o : p->parts) o->broken = true;
+      return r;
+    }
+  }
+  p->t_next += n;
+  if (where == PT_HOST) return group_finish(p);
+  return PT_OK;
+}
+
+int group_finish(pt_pipeline* p) {
+  int first_err = PT_OK;
+  std::string msg;
+  for (pt_pipeline* q : p->parts) {
+    DevGuard dg(q->device);
+    const int r = finish_impl(q);
+    if (r != PT_OK && first_err == PT_OK) {
+      first_err = r;
+      msg = g_err;
+    }
+  }
+  if (first_err != PT_OK) g_err = msg;
+  return first_err;
 }
 
 }  // namespace
@@ -1355,7 +1731,35 @@ int pt_create(const pt_config* cfg, pt_pipeline** out) {
   if (!out) return fail(PT_EINVAL, "out is null");
   *out = nullptr;
   pt_pipeline* p = new pt_pipeline();
-  int r = create_impl(cfg, p);
+  int r;
+  if (cfg && cfg->device_of_stage) {
+    // one device for every local stage: a plain handle on that device; several: a group
+    const int lo = cfg->local_stage_count ? cfg->local_stage_first : 0;
+    const int hi = cfg->local_stage_count ? lo + cfg->local_stage_count : cfg->n_stages;
+    bool one = true;
+    for (int h = lo + 1; h < hi && h < cfg->n_stages && lo >= 0; ++h)
+      one = one && cfg->device_of_stage[h] == cfg->device_of_stage[lo];
+    const char* ve = getenv("PT_VIRTUAL_DEVICES");
+    if (one && lo >= 0 && lo < cfg->n_stages && cfg->n_stages >= 1) {
+      int ndev = 1;
+      cudaGetDeviceCount(&ndev);
+      int d = cfg->device_of_stage[lo];
+      if (ve && atoi(ve) != 0 && ndev > 0) d %= ndev;
+      if (d < 0 || d >= ndev) {
+        r = fail(PT_EINVAL, "device_of_stage[" + std::to_string(lo) + "] = " + std::to_string(d) +
+                                " is not a device of this process");
+      } else {
+        pt_config sub = *cfg;
+        sub.device_of_stage = nullptr;
+        DevGuard dg(d);
+        r = create_impl(&sub, p);
+      }
+    } else {
+      r = create_group(cfg, p);
+    }
+  } else {
+    r = create_impl(cfg, p);
+  }
   if (r != PT_OK) {
     std::string keep = g_err;
     pt_destroy(p);
@@ -1368,7 +1772,19 @@ int pt_create(const pt_config* cfg, pt_pipeline** out) {
 
 void pt_destroy(pt_pipeline* p) {
   if (!p) return;
+  if (p->group()) {
+    for (pt_pipeline* q : p->parts) {
+      DevGuard dg(q->device);
+      cudaStreamSynchronize(q->stream);
+    }
+    for (pt_pipeline* q : p->parts) pt_destroy(q);
+    delete p;
+    return;
+  }
+  DevGuard dg(p->device);
+  resident_stop(p);
   cudaDeviceSynchronize();
+  if (p->res.host) cudaFreeHost(p->res.host);
   for (void* q : p->ipc_opened) cudaIpcCloseMemHandle(q);
   for (void* a : p->allocs)
     if (a) cudaFree(a);
@@ -1383,6 +1799,13 @@ int pt_set_params(pt_pipeline* p, int32_t layer, const float* W, const float* b,
   if (!p) return fail(PT_EINVAL, "null handle");
   BusyGuard g(p);
   if (!g.ok) return fail(PT_EBUSY, "contract violation: handle used concurrently");
+  if (p->group()) {
+    pt_pipeline* q = part_of_layer(p, layer);
+    if (!q) return fail(PT_EINVAL, "layer " + std::to_string(layer) + " is not owned by this process");
+    return pt_set_params(q, layer, W, b, where);
+  }
+  DevGuard dg(p->device);
+  PT_TRY(resident_stop(p));
   std::string why;
   LayerHost* Lh = local_layer(p, layer, &why);
   if (!Lh) return fail(PT_EINVAL, why);
@@ -1416,6 +1839,14 @@ int pt_get_params(pt_pipeline* p, int32_t layer, float* W, float* b, int32_t whe
   if (!p) return fail(PT_EINVAL, "null handle");
   BusyGuard g(p);
   if (!g.ok) return fail(PT_EBUSY, "contract violation: extract called mid-step (SPEC.md:239)");
+  if (p->group()) {
+    pt_pipeline* q = part_of_layer(p, layer);
+    if (!q) return fail(PT_EINVAL, "layer " + std::to_string(layer) + " is not owned by this process");
+    PT_TRY(group_finish(p));  // every part idle: the weights are a consistent tick
+    return pt_get_params(q, layer, W, b, where);
+  }
+  DevGuard dg(p->device);
+  PT_TRY(resident_stop(p));
   std::string why;
   LayerHost* Lh = local_layer(p, layer, &why);
   if (!Lh) return fail(PT_EINVAL, why);
@@ -1458,6 +1889,10 @@ int pt_run(pt_pipeline* p, const float* xs, const float* ys, int64_t n, float* o
   if (!p) return fail(PT_EINVAL, "null handle");
   BusyGuard g(p);
   if (!g.ok) return fail(PT_EBUSY, "contract violation: pipeline_step called concurrently (SPEC.md:221)");
+  if (where != PT_HOST && where != PT_DEVICE) return fail(PT_EINVAL, "where must be PT_HOST or PT_DEVICE");
+  if (p->group()) return group_run(p, xs, ys, n, outs, losses, valid, where);
+  DevGuard dg(p->device);
+  PT_TRY(resident_stop(p));
   return run_impl(p, xs, ys, n, outs, losses, valid, where);
 }
 
@@ -1468,18 +1903,24 @@ int pt_step(pt_pipeline* p, const float* x, const float* y, float* out, float* l
   if (!g.ok) return fail(PT_EBUSY, "contract violation: pipeline_step called concurrently (SPEC.md:221)");
   uint8_t v8 = 0;
   int r;
+  const bool grp = p->group();
+  pt_pipeline* last = grp ? p->parts.back() : p;
+  DevGuard dg(grp ? p->parts.front()->device : p->device);
+  if (!grp && where == PT_HOST && resident_eligible(p)) return resident_step(p, x, y, out, loss, valid);
+  if (!grp) PT_TRY(resident_stop(p));
   if (where == PT_HOST) {
-    r = run_impl(p, x, y, 1, out, loss, valid ? &v8 : nullptr, PT_HOST);
+    r = grp ? group_run(p, x, y, 1, out, loss, valid ? &v8 : nullptr, PT_HOST)
+            : run_impl(p, x, y, 1, out, loss, valid ? &v8 : nullptr, PT_HOST);
     if (valid) *valid = v8;
   } else {
     // device I/O: valid is int32 on the caller side; go through the staging byte
-    r = run_impl(p, x, y, 1, out, loss, nullptr, PT_DEVICE);
+    r = grp ? group_run(p, x, y, 1, out, loss, nullptr, PT_DEVICE) : run_impl(p, x, y, 1, out, loss, nullptr, PT_DEVICE);
     if (r == PT_OK) {
-      if (cudaStreamSynchronize(p->stream) != cudaSuccess) return fail(PT_ECUDA, "stream sync failed");
-      r = read_status(p);
-      if (valid && p->has_last()) {
+      r = grp ? group_finish(p) : finish_impl(p);
+      if (valid && last->has_last()) {
+        DevGuard dl(last->device);
         uint8_t hv = 0;
-        if (cudaMemcpy(&hv, p->valid_stage, 1, cudaMemcpyDeviceToHost) != cudaSuccess)
+        if (cudaMemcpy(&hv, last->valid_stage, 1, cudaMemcpyDeviceToHost) != cudaSuccess)
           return fail(PT_ECUDA, "valid copy failed");
         int32_t v32 = hv;
         if (cudaMemcpy(valid, &v32, 4, cudaMemcpyHostToDevice) != cudaSuccess)
@@ -1494,12 +1935,20 @@ int pt_sync(pt_pipeline* p) {
   if (!p) return fail(PT_EINVAL, "null handle");
   BusyGuard g(p);
   if (!g.ok) return fail(PT_EBUSY, "contract violation: handle used concurrently");
-  CUDA_TRY(cudaStreamSynchronize(p->stream));
-  return read_status(p);
+  if (p->group()) return group_finish(p);
+  DevGuard dg(p->device);
+  PT_TRY(resident_stop(p));
+  return finish_impl(p);
 }
 
 int pt_set_stream(pt_pipeline* p, void* stream) {
   if (!p) return fail(PT_EINVAL, "null handle");
+  if (p->group()) {
+    if (stream) return fail(PT_EUNSUPPORTED, "a multi-device handle runs one private stream per device");
+    return PT_OK;
+  }
+  DevGuard dg(p->device);
+  PT_TRY(resident_stop(p));
   CUDA_TRY(cudaStreamSynchronize(p->stream));
   p->stream = stream ? reinterpret_cast<cudaStream_t>(stream) : p->own_stream;
   return PT_OK;
@@ -1507,12 +1956,24 @@ int pt_set_stream(pt_pipeline* p, void* stream) {
 
 int pt_get_stream(const pt_pipeline* p, void** stream) {
   if (!p || !stream) return fail(PT_EINVAL, "null argument");
-  *stream = reinterpret_cast<void*>(p->stream);
+  // multi-device handle: the stream of the part that owns stage D (where outputs are written)
+  *stream = reinterpret_cast<void*>(p->group() ? p->parts.back()->stream : p->stream);
   return PT_OK;
 }
 
 int pt_last_kernel_ms(pt_pipeline* p, float* ms) {
   if (!p || !ms) return fail(PT_EINVAL, "null argument");
+  if (p->group()) {  // the slowest device
+    float worst = 0.f;
+    for (pt_pipeline* q : p->parts) {
+      float m = 0.f;
+      PT_TRY(pt_last_kernel_ms(q, &m));
+      worst = std::max(worst, m);
+    }
+    *ms = worst;
+    return PT_OK;
+  }
+  DevGuard dg(p->device);
   if (!p->timed) return fail(PT_EINVAL, "no kernel has run yet");
   CUDA_TRY(cudaEventSynchronize(p->ev1));
   CUDA_TRY(cudaEventElapsedTime(ms, p->ev0, p->ev1));
@@ -1521,13 +1982,27 @@ int pt_last_kernel_ms(pt_pipeline* p, float* ms) {
 
 int64_t pt_tick(pt_pipeline* p) { return p ? p->t_next : -1; }
 
+int32_t pt_stage_device(const pt_pipeline* p, int32_t stage) {
+  if (!p) return fail(PT_EINVAL, "null handle");
+  if (p->group()) {
+    for (const pt_pipeline* q : p->parts)
+      if (stage - 1 >= q->local_first && stage - 1 < q->local_first + q->local_count) return q->device;
+    return -1;
+  }
+  return (stage - 1 >= p->local_first && stage - 1 < p->local_first + p->local_count) ? p->device : -1;
+}
+
 int32_t pt_kernel_path(const pt_pipeline* p) {
   if (!p) return fail(PT_EINVAL, "null handle");
+  if (p->group()) return pt_kernel_path(p->parts.front());
   return p->tile ? PT_PATH_TILE : p->panel ? PT_PATH_PANEL : PT_PATH_TICK;
 }
 
 int pt_set_trace(pt_pipeline* p, int32_t cta, int32_t cap) {
   if (!p) return fail(PT_EINVAL, "null handle");
+  if (p->group()) return pt_set_trace(p->parts.front(), cta, cap);  // the stage-1 device
+  DevGuard dg(p->device);
+  PT_TRY(resident_stop(p));
   CUDA_TRY(cudaStreamSynchronize(p->stream));
   dev_free(p, p->d_trace);
   p->d_trace = nullptr;
@@ -1543,6 +2018,9 @@ int pt_set_trace(pt_pipeline* p, int32_t cta, int32_t cap) {
 
 int pt_get_trace(pt_pipeline* p, uint64_t* out, int32_t cap) {
   if (!p || !out) return fail(PT_EINVAL, "null argument");
+  if (p->group()) return pt_get_trace(p->parts.front(), out, cap);
+  DevGuard dg(p->device);
+  PT_TRY(resident_stop(p));
   if (!p->d_trace) return fail(PT_EINVAL, "tracing is off (pt_set_trace)");
   CUDA_TRY(cudaStreamSynchronize(p->stream));
   const int n = std::min(cap, p->trace_cap);
@@ -1553,6 +2031,9 @@ int pt_get_trace(pt_pipeline* p, uint64_t* out, int32_t cap) {
 int pt_ipc_export(pt_pipeline* p, int32_t stage, void* buf, size_t cap, size_t* len) {
   if (!p || !buf || !len) return fail(PT_EINVAL, "null argument");
   if (cap < sizeof(IpcBlob)) return fail(PT_EINVAL, "buffer too small");
+  if (p->group()) return fail(PT_EUNSUPPORTED, "export a stage of a single-device handle");
+  DevGuard dg(p->device);
+  PT_TRY(resident_stop(p));
   const int s = stage - 1 - p->local_first;
   if (s < 0 || s >= int(p->stages.size())) return fail(PT_EINVAL, "stage is not local");
   const StageHost& S = p->stages[s];
@@ -1578,6 +2059,9 @@ int pt_ipc_export(pt_pipeline* p, int32_t stage, void* buf, size_t cap, size_t* 
 int pt_ipc_import(pt_pipeline* p, const void* buf, size_t len) {
   if (!p || !buf) return fail(PT_EINVAL, "null argument");
   if (len < sizeof(IpcBlob)) return fail(PT_EINVAL, "IPC blob too short");
+  if (p->group()) return fail(PT_EUNSUPPORTED, "import into a single-device handle");
+  DevGuard dg(p->device);
+  PT_TRY(resident_stop(p));
   IpcBlob b;
   memcpy(&b, buf, sizeof(b));
   if (b.magic != PT_IPC_MAGIC || b.abi != PT_ABI_VERSION) return fail(PT_EINVAL, "not a partime IPC blob");

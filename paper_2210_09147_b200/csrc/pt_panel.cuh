@@ -109,6 +109,36 @@ struct PParams {
   u64* trace;
   int trace_cap, trace_cta;
   int jitter, jitter_mask;
+  // Resident per-sample mode (pt_step with host buffers): one launch serves every step until
+  // the host posts PN_STOP. The host writes x_t / gamma_t into mapped rings and then
+  // hreq = t + 1; CTA 0 relays hreq to the other CTAs through a device word; each CTA copies
+  // its slice of x_t into the tagged stage input xin[t & 1]; outputs go to the mapped
+  // rout[t & 1], and the CTA that arrives last at the end of tick t sums the loss partials (in
+  // the epilogue kernel's order) and publishes the PResDone record. No launch, no copy and no
+  // host round trip besides the two mapped words per step.
+  int resident;
+  const long long* hreq;  // host-mapped: ticks requested (t + 1), or PN_STOP
+  const int* hflag;       // host-mapped: 1 iff the step passed a target
+  long long* relay;       // device: CTA 0's copy of hreq for the other CTAs
+  const float* rx;        // host-mapped x ring [rring][ldx] (zero padded)
+  const float* ry;        // host-mapped target ring [rring][Fy]
+  int rring;
+  u64* xin;               // device: tagged stage-1 input [2][ldx]
+  float* rout;            // host-mapped outputs [2][F]
+  struct PResDone* rdone; // host-mapped completion record
+};
+
+constexpr long long PN_STOP = -1;
+
+// completion record of one resident step (written by the last CTA, read by the host)
+struct PResDone {
+  long long tick;        // t + 1 once the fields below belong to tick t
+  long long bad_loss;    // t if the loss was not finite, else -1
+  long long bad_target;  // first sample whose softmax-CE target is not a class index (int64 max: none)
+  float loss;
+  int valid;
+  int status;
+  int pad_;
 };
 
 __device__ __forceinline__ int cmod4(long long t) { return int(t & 3); }  // two's complement: -1 -> 3
@@ -128,6 +158,37 @@ __device__ __forceinline__ int pn_fbuf(const PParams& P, const PLayer& L, long l
 // the cache tick whose activations B(t) uses (act_delay reading)
 __device__ __forceinline__ long long pn_ct(const PParams& P, int h, long long t) {
   return (h < P.D && P.act_delay) ? t - 1 : t;
+}
+
+__device__ __forceinline__ long long ld_acquire_sys_s64(const long long* p) {
+  long long v;
+  asm volatile("ld.acquire.sys.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ long long ld_acquire_gpu_s64(const long long* p) {
+  long long v;
+  asm volatile("ld.acquire.gpu.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu_s64(long long* p, long long v) {
+  asm volatile("st.release.gpu.global.s64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ float ld_volatile_f32(const float* p) {
+  float v;
+  asm volatile("ld.volatile.global.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
+  return v;
+}
+// resident mode: wait until the host requested tick t (value >= t + 1) or posted a stop.
+// CTA 0 polls the mapped host word and relays it; the others poll the relay in L2.
+__device__ __forceinline__ bool pn_wait_request(const PParams& P, long long t, bool poll_host) {
+  long long r;
+  if (poll_host) {
+    while ((r = ld_acquire_sys_s64(P.hreq)) < t + 1 && r != PN_STOP) __nanosleep(64);
+    if (ld_acquire_gpu_s64(P.relay) != r) st_release_gpu_s64(P.relay, r);
+  } else {
+    while ((r = ld_acquire_gpu_s64(P.relay)) < t + 1 && r != PN_STOP) __nanosleep(32);
+  }
+  return r != PN_STOP;
 }
 
 __device__ __forceinline__ bool pn_watchdog(const PParams& P, uint64_t t_start) {
@@ -414,9 +475,15 @@ __device__ void pn_producer(const PParams& P, const PLayer* layers, const PStage
   };
   top_up();
   int raw_ti = 0;  // backward loads of ticks <= raw_ti may start (every CTA finished tick ti-1)
+  int req_ti = -1;  // resident mode: ticks <= req_ti were requested by the host
   while (!cur.done && !dead) {
     const int ti = cur.ti;
     const long long t = cur.t(P);
+    if (P.resident && ti > req_ti) {
+      // no load of a tick the host has not requested: at a stop, nothing is in flight
+      if (!pn_wait_request(P, t, false)) break;
+      req_ti = ti;
+    }
     if (P.learn && ti > 0) {
       if (cur.fwd() && !cur.L->bw) {
         // forward-written layer: my consumers stored my rows at tick ti-1; fenced yet?
@@ -488,7 +555,8 @@ struct PSmem {
   float* bias;  // own forward rows of every local layer's bias, resident for the launch
   int* boff;    // per layer: offset of its rows in `bias`
   int* blk;     // per layer: this CTA's row blocks [0, 1), column blocks [2, 3), input words [4, 5)
-  int* flags;   // [0] forward steps whose weight stores are fenced (producer's RAW wait)
+  int* flags;   // 32 ints: [0] forward steps whose weight stores are fenced (producer's RAW
+                // wait), [1] resident mode: the host posted a stop
   uint64_t* full;
   uint64_t* empty;
 };
@@ -603,8 +671,17 @@ __device__ __forceinline__ float pn_cta_red(float v, bool is_max, const PSmem& s
 // target row of sample sid (stage D): the run's ys or the target history ring
 __device__ __forceinline__ const float* pn_target(const PParams& P, long long sid, int Fy) {
   if (sid < 0) return nullptr;
+  if (sid >= P.t0 && P.resident) return P.ry + size_t(sid % P.rring) * Fy;
   if (sid >= P.t0) return P.ys ? P.ys + size_t(sid - P.t0) * Fy : nullptr;
   return P.yhist ? P.yhist + size_t(sid % P.yh) * Fy : nullptr;
+}
+
+// output row and loss partials of tick ti: per-run arrays, or two-tick rings (resident)
+__device__ __forceinline__ float* pn_outs(const PParams& P, int ti) {
+  return P.resident ? P.rout + size_t(ti & 1) * P.F : P.outs + size_t(ti) * P.F;
+}
+__device__ __forceinline__ float* pn_lpart(const PParams& P, int ti) {
+  return P.loss_part + size_t(P.resident ? (ti & 1) : ti) * P.G;
 }
 
 // wait for one ring slot's data (consumer threads); the slot / phase cursor advances
@@ -621,6 +698,43 @@ __device__ __forceinline__ int pn_take(const PSmem& sm, int& cslot, uint32_t& cp
       if (pn_watchdog(P, t0)) break;
   }
   return slot;
+}
+
+// Resident mode, last CTA of tick t: the epilogue kernel's loss (same summation order:
+// lane-strided partial sums, then the xor butterfly of warp_sum), validity, the non-finite
+// check, then the record's tick word last.
+__device__ __noinline__ void pn_resident_done(const PParams& P, long long t, int ti) {
+  __threadfence();
+  const bool have = ld_volatile_s32(P.hflag) != 0;
+  const bool v = t >= P.D - 1;
+  float s = 0.f;
+  if (v && have) {
+    const float* lp = pn_lpart(P, ti);
+    float acc[32];
+#pragma unroll
+    for (int l = 0; l < 32; ++l) {
+      float a = 0.f;
+      for (int c = l; c < P.G; c += 32) a += ldcg(lp + c);
+      acc[l] = a;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      float nx[32];
+#pragma unroll
+      for (int l = 0; l < 32; ++l) nx[l] = acc[l] + acc[l ^ o];
+#pragma unroll
+      for (int l = 0; l < 32; ++l) acc[l] = nx[l];
+    }
+    s = acc[0] * (P.loss == 1 ? 1.f : 1.f / float(P.F));
+  }
+  PResDone* d = P.rdone;
+  d->loss = (v && have) ? s : __int_as_float(0x7fc00000);
+  d->valid = v ? 1 : 0;
+  d->bad_loss = (v && have && !isfinite(s)) ? t : -1;
+  d->bad_target = *reinterpret_cast<volatile long long*>(P.bad_target);
+  d->status = ld_volatile_s32(P.status);
+  __threadfence_system();
+  *reinterpret_cast<volatile long long*>(&d->tick) = t + 1;
 }
 
 template <int DUMMY>
@@ -735,6 +849,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constan
   for (int ti = 0; ti < P.n; ++ti) {
     const long long t = P.t0 + ti;
     const uint32_t tag_t = tag_of_tick(t);
+    if (P.resident) {
+      if (tid == 0) sm.flags[1] = pn_wait_request(P, t, c == 0) ? 0 : 1;
+      cons_sync(NCT);
+      if (sm.flags[1]) break;
+      if (s_stages[0].h == 1) {
+        // this CTA's slice of x_t: mapped host memory -> the tagged stage-1 input
+        const int* bk0 = sm.blk + 6 * s_stages[0].first;
+        const float* xr = P.rx + size_t(t % P.rring) * P.ldx;
+        u64* xd = P.xin + size_t(t & 1) * P.ldx;
+        for (int j = bk0[4] + tid; j < bk0[5]; j += NCT) st_tv_gpu(xd + j, pack_tv(ld_volatile_f32(xr + j), tag_t));
+      }
+    }
     // tick barrier. Learning: every CTA finished tick t-1 (orders this tick's weight stores
     // after every read of their buffer, and keeps per-tick rings one tick deep). Inference:
     // lagged by one tick (cache slots only).
@@ -765,6 +891,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constan
         // the input vector (the dependency): loads in flight now, resolved after the update
         PV vin{nullptr, 0u, 0};
         if (i == 0 && h > 1) vin = PV{S.inslot[(t - 1) & 1], tag_of_tick(t - 1), S.up_remote};
+        else if (i == 0 && P.resident) vin = PV{P.xin + size_t(t & 1) * P.ldx, tag_t, 0};
         else if (i > 0) vin = PV{Ccur + L.cache_in, tag_t, 0};
         PBatch dep;
         dep.issue(vin, nin, 0);
@@ -814,7 +941,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constan
           }
         }
         // the input
-        if (i == 0 && h == 1) {
+        if (i == 0 && h == 1 && !P.resident) {
           const float* x = P.xs + size_t(ti) * P.ldx;
           for (int j = tid * 4; j < nin; j += NCT * 4)
             *reinterpret_cast<float4*>(sm.va + j) = ldcg4(reinterpret_cast<const float4*>(x + j));
@@ -913,7 +1040,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constan
               else st_tv_gpu(S.peer_inslot[t & 1] + row, w);
             }
             if (net_last && row < P.F) {
-              P.outs[size_t(ti) * P.F + row] = a;
+              pn_outs(P, ti)[row] = a;
               if (P.loss == 0 && y) {
                 const float d = a - y[row];
                 lsum = fmaf(d, d, lsum);
@@ -927,7 +1054,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constan
           // MSE: this CTA's partial of sum (a - y)^2 (the epilogue divides by M*F); softmax-CE:
           // CTA 0 writes the loss after the full output is gathered (backward, or below)
           lsum = warp_sum(lsum);
-          if (lane == 0) P.loss_part[size_t(ti) * G + c] = lsum;
+          if (lane == 0) pn_lpart(P, ti)[c] = lsum;
         }
         PN_TR(4);
         if (net_last && P.loss == 1 && !P.learn && c == 0 && y) {
@@ -948,9 +1075,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constan
             const int tgt = int(y[0]);
             if (!(y[0] >= 0.f && y[0] < float(P.F) && float(tgt) == y[0])) {
               atomicMin(P.bad_target, sid);
-              P.loss_part[size_t(ti) * G] = 0.f;
+              pn_lpart(P, ti)[0] = 0.f;
             } else {
-              P.loss_part[size_t(ti) * G] = mx + logf(se) - sm.va[tgt];
+              pn_lpart(P, ti)[0] = mx + logf(se) - sm.va[tgt];
             }
           }
         }
@@ -1029,7 +1156,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constan
           }
           if (c == 0 && tid == 0 && y) {
             if (!ok) atomicMin(P.bad_target, sid);
-            P.loss_part[size_t(ti) * G] = ok ? lse - sm.va[tgt] : 0.f;
+            pn_lpart(P, ti)[0] = ok ? lse - sm.va[tgt] : 0.f;
           }
           cons_sync(NCT);  // thread 0 read va[tgt] before it is rewritten
           for (int f = tid; f < nout; f += NCT) {
@@ -1125,8 +1252,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constan
     if (P.learn) fence_proxy_async_global();
     cons_sync(NCT);
     if (tid == 0) {
-      __threadfence();
-      red_release_gpu(P.tick_end, 1);
+      if (P.resident) {
+        // outputs went to host memory: make them visible system-wide before arriving; the
+        // last CTA to arrive completes the step for the host
+        __threadfence_system();
+        const u64 old = atomicAdd(reinterpret_cast<unsigned long long*>(P.tick_end), 1ull);
+        if (old + 1 == u64(G) * u64(t + 1)) pn_resident_done(P, t, ti);
+      } else {
+        __threadfence();
+        red_release_gpu(P.tick_end, 1);
+      }
     }
     PN_TR(20);
   }

@@ -77,6 +77,33 @@ def _is_cuda(a):
     return torch is not None and isinstance(a, torch.Tensor) and a.is_cuda
 
 
+def device_map(devices, D):
+    """Stage -> CUDA device ordinal for a `devices` list (one device per stage for
+    maximum performance, or fewer, "making multiple stages execute on the same device"). With
+    fewer devices than stages, device k takes a contiguous block of stages (k*D//n .. ), so that
+    the stages of one device stay contiguous. None -> None (the current device)."""
+    if devices is None:
+        return None
+    devs = list(devices)
+    if not devs:
+        return None
+    if len(devs) > D:
+        raise ValueError(f"{len(devs)} devices for {D} stages: at most one device per stage")
+    ords = []
+    for d in devs:
+        if isinstance(d, int):
+            ords.append(d)
+            continue
+        if torch is None:
+            raise ValueError(f"device {d!r}: give CUDA device ordinals without torch")
+        td = torch.device(d)
+        if td.type != "cuda":
+            raise ValueError(f"device {d!r} is not a CUDA device (the B200 engine has no CPU path)")
+        ords.append(td.index if td.index is not None else torch.cuda.current_device())
+    n = len(ords)
+    return [ords[h * n // D] for h in range(D)]
+
+
 def _f32(a):
     if torch is not None and isinstance(a, torch.Tensor):
         return a.detach().to(torch.float32).contiguous()
@@ -87,7 +114,7 @@ class Pipeline:
     """D-stage PARTIME pipeline on B200 (pipeline_build)."""
 
     def __init__(self, model: Model, plan, optimizer="sgd", lr=1e-3, sample_input=None, sample_target=None,
-                 act_delay=1, learn=True, grid=0, local_stages=None, timeout_ms=0):
+                 act_delay=1, learn=True, grid=0, local_stages=None, timeout_ms=0, devices=None):
         lib = _lib.load()
         units, owner = fuse(model)
         if isinstance(plan, (list, tuple)):
@@ -134,6 +161,8 @@ class Pipeline:
         if local_stages is None:
             local_stages = (0, self.D)
         self.local_first, self.local_count = local_stages
+        self.device_of_stage = device_map(devices, self.D)
+        dev_i = None if self.device_of_stage is None else (ctypes.c_int32 * self.D)(*self.device_of_stage)
         D_i = (ctypes.c_int32 * len(dims))(*dims)
         A_i = (ctypes.c_int32 * self.L)(*[_lib.PT_ACT[u[1]] for u in units])
         S_i = (ctypes.c_int32 * len(sfl))(*sfl)
@@ -141,10 +170,17 @@ class Pipeline:
             n_layers=self.L, dims=D_i, act=A_i, loss=_lib.PT_LOSS[model.loss], optimizer=_lib.PT_OPT[optimizer],
             lr=self.lr, n_stages=self.D, stage_first_layer=S_i, batch=self.M, learn=int(self.learn),
             act_delay=self.act_delay, local_stage_first=self.local_first, local_stage_count=self.local_count,
-            grid=int(grid), timeout_ms=int(timeout_ms))
+            grid=int(grid), timeout_ms=int(timeout_ms), device_of_stage=dev_i)
         h = ctypes.c_void_p()
         _lib.check(lib.pt_create(ctypes.byref(cfg), ctypes.byref(h)), "pipeline_build")
         self._h = h
+        # devices of this process's stages (several: one handle drives one part per device)
+        local = range(self.local_first + 1, self.local_first + self.local_count + 1)
+        self.stage_devices = {s: int(lib.pt_stage_device(h, s)) for s in local}
+        # one handle driving several devices (PT_VIRTUAL_DEVICES may map them onto one GPU, so
+        # this follows the requested map; stage_devices holds the physical ordinals)
+        self.multi_device = self.device_of_stage is not None and len(
+            {self.device_of_stage[s - 1] for s in local}) > 1
         self._lib = lib
         self._t = 0
         self._user_stream = False
@@ -224,7 +260,8 @@ class Pipeline:
         if y is not None and not dev:
             self._check_targets(y, f"step {self._t}")
         if dev:
-            out = torch.empty((M, F), dtype=torch.float32, device=x.device if x is not None else y.device)
+            x, y = self._place(x, y)
+            out = torch.empty((M, F), dtype=torch.float32, device=self._out_device(x, y))
             loss = torch.empty(1, dtype=torch.float32, device=out.device)
             valid = torch.empty(1, dtype=torch.int32, device=out.device)
             where = _lib.PT_DEVICE
@@ -261,8 +298,8 @@ class Pipeline:
         if ys is not None and not dev:
             self._check_targets(ys, f"steps [{self._t}, {self._t + n})")
         if dev:
-            d = xs.device if xs is not None else (ys.device if ys is not None else
-                                                   torch.device("cuda", torch.cuda.current_device()))
+            xs, ys = self._place(xs, ys)
+            d = self._out_device(xs, ys)
             outs = torch.empty((n, M, F), dtype=torch.float32, device=d)
             losses = torch.empty(n, dtype=torch.float32, device=d)
             valid = torch.empty(n, dtype=torch.uint8, device=d)
@@ -312,6 +349,23 @@ class Pipeline:
         _lib.check(self._lib.pt_sync(self._h), "sync")
 
     # ---- stream ordering with torch (device buffers) ---------------------------------------
+    def _place(self, x, y):
+        """Device inputs of a multi-device pipeline: x on stage 1's device, targets on stage D's."""
+        if not self.multi_device:
+            return x, y
+        if x is not None and 1 in self.stage_devices:
+            x = x.to(torch.device("cuda", self.stage_devices[1]))
+        if y is not None and self.D in self.stage_devices:
+            y = y.to(torch.device("cuda", self.stage_devices[self.D]))
+        return x, y
+
+    def _out_device(self, x, y):
+        if self.D in self.stage_devices:
+            return torch.device("cuda", self.stage_devices[self.D])
+        if x is not None:
+            return x.device
+        return y.device if y is not None else torch.device("cuda", torch.cuda.current_device())
+
     def _stream(self, device):
         raw = ctypes.c_void_p()
         _lib.check(self._lib.pt_get_stream(self._h, ctypes.byref(raw)), "get_stream")
@@ -319,7 +373,12 @@ class Pipeline:
 
     def _order_after_torch(self, device):
         """Device inputs were written on torch's current stream (e.g. an async H2D copy):
-        the handle's stream waits for it before the kernel reads them."""
+        the handle's stream waits for it before the kernel reads them. A multi-device handle
+        runs one private stream per device: torch's streams on those devices are drained."""
+        if self.multi_device:
+            for d in sorted(set(self.stage_devices.values())):
+                torch.cuda.current_stream(torch.device("cuda", d)).synchronize()
+            return
         self._stream(device).wait_stream(torch.cuda.current_stream(device))
 
     def _order_torch_after(self, device):

@@ -17,7 +17,7 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
-from ..engine import Pipeline as _Engine
+from ..engine import Pipeline as _Engine, device_map
 from ..model import StagePlan
 from .convert import sequential_to_model
 
@@ -63,23 +63,29 @@ class Pipeline:
                 raise NotImplementedError(f"optimizer {cls.__name__} is not implemented on the B200 path")
             lr = float(hp.get("lr", lr))
         devs = [torch.device(d) for d in devices] if devices else [torch.device("cuda", torch.cuda.current_device())]
-        if len({(d.type, d.index if d.index is not None else torch.cuda.current_device()) for d in devs}) != 1:
-            raise NotImplementedError("stages on several GPUs run one process per GPU "
-                                      "(paper_2210_09147_b200.dist.build_distributed); a single process "
-                                      "drives one device")
-        self.device = devs[0]
+        devs = [torch.device("cuda", d.index if d.index is not None else torch.cuda.current_device())
+                if d.type == "cuda" else d for d in devs]
+        # stage -> device: one device per stage, or fewer devices each taking a contiguous block
+        # of stages; several devices are driven from this process by one handle
+        # (peer access, NVLink peer stores between neighbouring stages)
+        dmap = device_map(devs, len(balance))
+        self.devices = devs
         self.net = net
         model = sequential_to_model(net)
         model.loss = loss
         plan = StagePlan.from_counts(list(balance))
         si = sample_input.detach().cpu().numpy() if hasattr(sample_input, "detach") else sample_input
         st = sample_target.detach().cpu().numpy() if hasattr(sample_target, "detach") else sample_target
-        with torch.cuda.device(self.device):
-            self._eng = _Engine(model, plan, opt, lr, si, st, act_delay=act_delay)
+        self._eng = _Engine(model, plan, opt, lr, si, st, act_delay=act_delay, devices=dmap)
+        # physical devices of the stages (the engine reports them; PT_VIRTUAL_DEVICES may fold
+        # the requested ordinals onto fewer GPUs)
+        phys = self._eng.stage_devices
+        self.device = torch.device("cuda", phys[len(balance)])  # outputs_buffer / loss_buffer: with stage D
+        self.input_device = torch.device("cuda", phys[1])
         mods = list(net)
         self.stages, a = [], 0
         for h, c in enumerate(balance):
-            self.stages.append(Stage(h, mods[a:a + c], devs[min(h, len(devs) - 1)]))
+            self.stages.append(Stage(h, mods[a:a + c], torch.device("cuda", phys[h + 1])))
             a += c
         shape = (self._eng.F,) if self._eng._squeeze else (self._eng.M, self._eng.F)
         self.outputs_buffer = torch.zeros(shape, device=self.device)
@@ -90,7 +96,7 @@ class Pipeline:
         """One tick: forward, push, delayed backward and update on every stage (Alg. 1)."""
         import torch
 
-        inp = inp.to(self.device) if hasattr(inp, "to") else torch.as_tensor(inp, device=self.device)
+        inp = inp.to(self.input_device) if hasattr(inp, "to") else torch.as_tensor(inp, device=self.input_device)
         if target is not None:
             target = target.to(self.device) if hasattr(target, "to") else torch.as_tensor(target, device=self.device)
         out = self._eng.step(inp, target)

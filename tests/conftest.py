@@ -10,6 +10,8 @@ if ROOT not in sys.path:
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (sm_100a) GPU")
+    config.addinivalue_line("markers", "gpu2: needs two or more GPUs in one process (skips otherwise); "
+                                       "always also marked gpu")
 
 
 def _has_gpu():

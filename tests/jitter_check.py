@@ -12,12 +12,15 @@ import numpy as np  # noqa: E402
 from paper_2210_09147_b200 import engine, model as mdl, streams  # noqa: E402
 
 CASES = {"tile": ([256, 512, 512, 256, 256], 16), "tick": ([32, 64, 64, 64, 16], 1),
+         "panel": ([32, 64, 64, 64, 16], 1), "panel_wide": ([256, 512, 512, 512, 128], 1),
          "tick_mb": ([64, 96, 96, 96, 32], 4), "tick_conc": ([256] * 9, 1), "tick_conc_mb": ([128] * 9, 4),
          "tick_mb_wide": ([1218, 3805, 2590, 1500], 2)}
 
 
 def main(kind, counts, learn):
     widths, M = CASES[kind]
+    if kind.startswith("tick"):
+        os.environ["PT_PANEL"] = "0"  # the row-owned tick kernel (batch 1 defaults to the panel kernel)
     T = 16
     st = streams.SmoothStream(widths[0], widths[-1], seed=5, batch=M)
     xs, ys = st.block(0, T)
@@ -26,7 +29,7 @@ def main(kind, counts, learn):
 
     def run():
         p = engine.Pipeline(mdl.mlp(widths, seed=4), counts, "sgd", 0.05, s0(xs), s0(ys), learn=learn)
-        assert p.kernel_path == ("tile" if kind == "tile" else "tick"), p.kernel_path
+        assert p.kernel_path == kind.split("_")[0], p.kernel_path
         o, l, _ = p.run(xs, ys)
         W = [p.get_layer(j)[0] for j in range(p.L)]
         p.close()

@@ -25,7 +25,7 @@ def test_header_symbols_exported():
     assert set(syms) == set(_lib.EXPORTS)
     for s in syms:
         assert hasattr(lib, s), s
-    assert lib.pt_abi_version() == 1
+    assert lib.pt_abi_version() == 2
 
 
 def _cfg(dims, D_first, act=None, batch=1, **kw):

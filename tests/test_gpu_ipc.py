@@ -39,7 +39,7 @@ def test_ipc_stage_handles_match_single_handle(widths, counts, T, M, grid):
     xs, ys = st.block(0, T)
     xs, ys = xs.astype(np.float32), ys.astype(np.float32)
     m, a, b = _stage_pair(widths, counts, 0.05, xs, ys, grid=grid, M=M)
-    assert a.kernel_path == b.kernel_path == ("tile" if M == 16 else "tick")
+    assert a.kernel_path == b.kernel_path == ("tile" if M == 16 else "panel")
     sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
     a.set_stream(sa)
     b.set_stream(sb)
@@ -60,17 +60,19 @@ def test_ipc_stage_handles_match_single_handle(widths, counts, T, M, grid):
         p.close()
 
 
-def test_concurrent_stages_match_two_handles():
-    """One handle with two local stages of equal bytes runs them concurrently, 74 CTAs each
+def test_concurrent_stages_match_two_handles(monkeypatch):
+    """The row-owned tick kernel (PT_PANEL=0). One handle with two local stages of equal bytes runs them concurrently, 74 CTAs each
     (DESIGN.md §4.1). Its result must equal two co-resident single-stage handles of 74 CTAs
     exchanging through the IPC path, bit for bit: the same row split, the same protocol."""
     import torch
     from paper_2210_09147_b200 import engine, model as mdl, streams
+    monkeypatch.setenv("PT_PANEL", "0")
     widths, counts, T = [256] * 7, [6, 5], 16  # 3 + 3 dense layers of 256 x 256
     st = streams.SmoothStream(widths[0], widths[-1], seed=5)
     xs, ys = st.block(0, T)
     xs, ys = xs.astype(np.float32), ys.astype(np.float32)
     m, a, b = _stage_pair(widths, counts, 0.05, xs, ys, grid=74)
+    assert a.kernel_path == b.kernel_path == "tick"
     sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
     a.set_stream(sa)
     b.set_stream(sb)

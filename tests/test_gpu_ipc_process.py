@@ -15,8 +15,9 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 # (widths, counts, ticks, batch)
-CASES = {"tick": ([32, 64, 64, 64, 16], [4, 3], 12, 1),
-         "tick_wide": ([256, 512, 512, 512, 128], [4, 3], 24, 1),
+CASES = {"panel": ([32, 64, 64, 64, 16], [4, 3], 12, 1),
+         "panel_wide": ([256, 512, 512, 512, 128], [4, 3], 24, 1),
+         "tick": ([32, 64, 64, 64, 16], [4, 3], 12, 1),
          "tick_microbatch": ([64, 96, 96, 96, 32], [4, 3], 16, 4),
          "tile": ([256, 512, 512, 256, 256], [4, 3], 12, 16)}
 
@@ -34,6 +35,8 @@ def _sample(a, M):
 
 
 def _worker(rank, port, q, case):
+    if case.startswith("tick"):
+        os.environ["PT_PANEL"] = "0"  # the row-owned tick kernel
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE="2")
     import torch
     import torch.distributed as dist
@@ -70,19 +73,22 @@ def test_two_process_ipc_matches_single_process(case):
         p.start()
     got = {}
     for _ in procs:
-        r = q.get(timeout=300)
+        r = q.get(timeout=150)
         got[r["rank"]] = r
     for p in procs:
         p.join(timeout=120)
     widths, counts, T, M, xs, ys = _data(case)
-    assert got[0]["path"] == got[1]["path"] == ("tile" if M == 16 else "tick")
+    assert got[0]["path"] == got[1]["path"] == case.split("_")[0]
     # the single-process reference runs its two stages in turn on the whole grid, like each
     # process does with its one stage
     os.environ["PT_CONC"] = "0"
+    if case.startswith("tick"):
+        os.environ["PT_PANEL"] = "0"
     try:
         ref = engine.Pipeline(mdl.mlp(widths, seed=4), counts, "sgd", 0.05, _sample(xs, M), _sample(ys, M))
     finally:
         os.environ.pop("PT_CONC", None)
+        os.environ.pop("PT_PANEL", None)
     o, l, v = ref.run(xs, ys)
     assert np.array_equal(got[1]["outs"], o) and np.array_equal(got[1]["losses"], l, equal_nan=True)
     W = [ref.get_layer(j) for j in range(ref.L)]

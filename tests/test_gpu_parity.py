@@ -112,6 +112,67 @@ def test_step_api_matches_run():
         assert all(np.array_equal(u, v) for u, v in zip(a.get_layer(j), b.get_layer(j)))
 
 
+@pytest.mark.parametrize("loss", ["mse", "softmax_ce"])
+def test_resident_steps_interleaved_with_runs(loss):
+    """Per-sample steps run in one resident launch (pt_step, host buffers, panel kernel); runs,
+    weight reads and writes in between stop and restart it. Any interleaving equals one
+    pt_run over the same stream, bit for bit (targets queued across the switches)."""
+    widths, counts, T = [48, 80, 80, 80, 10], [2, 2, 3], 30
+    m = mdl.mlp(widths, seed=7, loss=loss)
+    st = streams.SmoothStream(widths[0], widths[-1], seed=8)
+    xs, ys = st.block(0, T)
+    if loss == "softmax_ce":
+        ys = np.argmax(ys, axis=-1).astype(np.float64)[..., None]
+    xs, ys = xs.astype(np.float32), ys.astype(np.float32)
+    mk = lambda: engine.Pipeline(m, counts, "sgd", 0.05, xs[0, 0], ys[0, 0])
+    a, b = mk(), mk()
+    assert b.kernel_path == "panel"
+    o_ref, l_ref, v_ref = a.run(xs, ys)
+    outs, losses = [], []
+    t = 0
+    for seg, kind in ((5, "step"), (4, "run"), (7, "step"), (3, "get"), (6, "step"), (5, "run")):
+        if kind == "get":
+            W, bias = b.get_layer(1)
+            b.set_layer(1, W, bias)  # a round trip through the tiled layout is exact
+            seg = 0
+        elif kind == "run":
+            o, l, _ = b.run(xs[t:t + seg], ys[t:t + seg])
+            outs += list(o[:, 0])
+            losses += list(l)
+        else:
+            for k in range(seg):
+                r = b.step(xs[t + k, 0], ys[t + k, 0])
+                outs.append(r.output)
+                losses.append(np.nan if r.loss is None else r.loss)
+                assert r.valid == bool(v_ref[t + k])
+        t += seg
+    assert t == T
+    assert np.array_equal(np.array(outs), o_ref[:, 0])
+    assert np.array_equal(np.array(losses, np.float32), l_ref, equal_nan=True)
+    for j in range(a.L):
+        assert all(np.array_equal(u, v) for u, v in zip(a.get_layer(j), b.get_layer(j)))
+    a.close()
+    b.close()
+
+
+def test_resident_step_errors():
+    """The resident path reports a non-finite loss with its step and a softmax-CE
+    target outside [0, F), like pt_run."""
+    m = mdl.mlp([16, 32, 4], seed=1, loss="softmax_ce")
+    p = engine.Pipeline(m, [3], "sgd", 0.05, np.zeros(16, np.float32), np.zeros(1, np.float32))
+    p.step(np.ones(16, np.float32), np.array([1.0], np.float32))
+    with pytest.raises(ValueError, match="class range"):
+        p.step(np.ones(16, np.float32), np.array([7.0], np.float32))
+    p.close()
+    m = mdl.mlp([16, 32, 4], seed=1)
+    p = engine.Pipeline(m, [3], "sgd", 0.05, np.zeros(16, np.float32), np.zeros(4, np.float32))
+    p.step(np.ones(16, np.float32), np.zeros(4, np.float32))
+    from paper_2210_09147_b200._lib import NonFiniteLoss
+    with pytest.raises(NonFiniteLoss, match="step 1"):
+        p.step(np.full(16, np.inf, np.float32), np.zeros(4, np.float32))
+    p.close()
+
+
 def test_run_split_across_calls():
     """Targets queued across pt_run calls: 3 calls == 1 call, bit for bit."""
     m, st, mk = _pipe([16, 32, 32, 32, 8], [2, 2, 3], 0.05)
