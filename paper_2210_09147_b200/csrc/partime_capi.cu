@@ -858,6 +858,15 @@ int create_impl(const pt_config* c, pt_pipeline* p) {
                          (const void*)pt::tick_kernel<false, 4, true>, (const void*)pt::tick_kernel<false, 8, true>};
     for (const void* f : fns)
       CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, pt::SMEM_MAX));
+    // Load every kernel of the library now. With lazy module loading (the CUDA default) the
+    // first launch of a kernel may wait for the kernels running on the device; a persistent
+    // stage kernel waiting for a neighbour (another handle, part or process) that is itself
+    // blocked in such a load would only end at the watchdog.
+    const void* others[] = {(const void*)pt::panel_kernel<0>, (const void*)pt::tile_kernel,
+                            (const void*)pt::epilogue_kernel, (const void*)pt::pn_to_tiles,
+                            (const void*)pt::pn_from_tiles};
+    cudaFuncAttributes fa;
+    for (const void* f : others) CUDA_TRY(cudaFuncGetAttributes(&fa, f));
   }
   int per_sm = 0;
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pt::tick_kernel<true, 8, false>, pt::NTHREADS,

@@ -310,19 +310,12 @@ class Pipeline:
             valid = np.empty(n, np.uint8)
             where = _lib.PT_HOST
         has_last = self.local_first + self.local_count == self.D
-        order = dev and not self._user_stream
-        if order:
-            self._order_after_torch(outs.device)
-        rc = self._lib.pt_run(self._h, _ptr(xs), _ptr(ys), n, _ptr(outs) if has_last else None,
-                              _ptr(losses) if has_last else None, _ptr(valid) if has_last else None, where)
-        if order:
-            self._order_torch_after(outs.device)
         t0 = self._t
-        self._t += n
-        _lib.check(rc, f"pipeline_run at steps [{t0}, {t0 + n})")
         if not has_last:
             # this process does not own stage D: no outputs or losses here, but validity is
-            # known from the tick alone
+            # known from the tick alone. Filled before the launch: a torch
+            # kernel launched while the pipeline runs may need a lazy module load, which waits
+            # for the running kernels, while they wait for a neighbour that has not launched yet
             ticks = np.arange(t0, t0 + n)
             if dev:
                 valid.copy_(torch.from_numpy((ticks >= self.D - 1).astype(np.uint8)))
@@ -332,6 +325,15 @@ class Pipeline:
                 valid[:] = ticks >= self.D - 1
                 losses[:] = np.nan
                 outs[:] = np.nan
+        order = dev and not self._user_stream
+        if order:
+            self._order_after_torch(outs.device)
+        rc = self._lib.pt_run(self._h, _ptr(xs), _ptr(ys), n, _ptr(outs) if has_last else None,
+                              _ptr(losses) if has_last else None, _ptr(valid) if has_last else None, where)
+        if order:
+            self._order_torch_after(outs.device)
+        self._t += n
+        _lib.check(rc, f"pipeline_run at steps [{t0}, {t0 + n})")
         return outs, losses, valid
 
     def _check_targets(self, y, where):

@@ -41,6 +41,38 @@ def run_oracle(m, counts, xs, ys, lr, dtype=np.float64, act_delay=1, learn=True,
     return np.array(outs), np.array(losses), np.array(valid), W, b
 
 
+def run_oracle_permuted(m, counts, xs, ys, lr, dtype, act_delay, learn, loss, optimizer, seed):
+    """The oracle on a mathematically identical network whose hidden units are permuted
+    (rows of W_l and b_l, columns of W_{l+1}): the same function, but every dot product sums
+    in another order, so it is another equally valid f32 evaluation. Weights are returned in
+    the original unit order."""
+    import copy
+    rng = np.random.default_rng(seed)
+    dense = [i for i, l in enumerate(m.layers) if l.kind == "dense"]
+    perms = [rng.permutation(m.layers[i].out_dim) for i in dense[:-1]]
+    mp = copy.copy(m)
+    mp.layers = [copy.copy(l) for l in m.layers]
+    for j, i in enumerate(dense):
+        W, b = np.array(m.layers[i].W), np.array(m.layers[i].b)
+        if j < len(perms):
+            W, b = W[perms[j]], b[perms[j]]
+        if j > 0:
+            W = W[:, perms[j - 1]]
+        mp.layers[i].W, mp.layers[i].b = W, b
+    o, l, v, Wp, bp = run_oracle(mp, counts, xs, ys, lr, dtype, act_delay, learn, loss, optimizer)
+    W, bb = [], []
+    for j in range(len(dense)):
+        w, b = Wp[j], bp[j]
+        if j < len(perms):
+            inv = np.argsort(perms[j])
+            w, b = w[inv], b[inv]
+        if j > 0:
+            w = w[:, np.argsort(perms[j - 1])]
+        W.append(w)
+        bb.append(b)
+    return o, l, v, W, bb
+
+
 def rel(a, b):
     a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
     return float(np.max(np.abs(a - b)) / (np.max(np.abs(b)) + 1e-30))

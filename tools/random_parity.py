@@ -32,10 +32,15 @@ def random_case(rng, wmax=None):
         u += c
     assert sum(counts) == n_layers
     loss = "softmax_ce" if rng.random() < 0.3 and widths[-1] >= 2 else "mse"
-    return dict(widths=widths, counts=counts, T=int(rng.integers(2 * D + 2, 24)), lr=float(rng.choice([0.0, 0.01, 0.05])),
+    c = dict(widths=widths, counts=counts, T=int(rng.integers(2 * D + 2, 24)), lr=float(rng.choice([0.0, 0.01, 0.05])),
                 act=str(rng.choice(["relu", "tanh"])), act_delay=int(rng.integers(0, 2)), M=M,
                 optimizer=("sgd" if os.environ.get("TILE_ONLY") else str(rng.choice(["sgd", "sgd", "adam"]))), loss=loss, seed=int(rng.integers(0, 1000)),
                 learn=bool(rng.random() >= float(os.environ.get("P_INFER", "0"))))
+    if os.environ.get("OPT"):  # e.g. OPT=adam LR=0.05: the Adam cases at the largest lr
+        c["optimizer"] = os.environ["OPT"]
+    if os.environ.get("LR"):
+        c["lr"] = float(os.environ["LR"])
+    return c
 
 
 if __name__ == "__main__":
