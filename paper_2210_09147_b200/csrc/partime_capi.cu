@@ -12,6 +12,7 @@
 
 #include <atomic>
 #include <chrono>
+#include <thread>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -1246,7 +1247,22 @@ int resident_stop(pt_pipeline* p) {
   *reinterpret_cast<volatile long long*>(r.req) = pt::PN_STOP;
   std::atomic_thread_fence(std::memory_order_seq_cst);
   r.on = false;
-  CUDA_TRY(cudaStreamSynchronize(p->stream));
+  {
+    // the launch ends at its next tick boundary; never block without a bound on it
+    const auto t_begin = std::chrono::steady_clock::now();
+    cudaError_t q;
+    while ((q = cudaStreamQuery(p->stream)) == cudaErrorNotReady) {
+      if (std::chrono::steady_clock::now() - t_begin > std::chrono::nanoseconds(2 * p->timeout_ns)) {
+        long long relay = 0;
+        cudaMemcpy(&relay, r.relay, sizeof(relay), cudaMemcpyDeviceToHost);
+        p->broken = true;
+        return fail(PT_ETIMEOUT, "resident launch did not stop (relay " + std::to_string(relay) + ", tick " +
+                                     std::to_string(p->t_next) + ")");
+      }
+      std::this_thread::yield();
+    }
+    if (q != cudaSuccess) return fail(PT_ECUDA, std::string("resident launch failed: ") + cudaGetErrorString(q));
+  }
   const int Fy = p->Fy();
   for (long long s = std::max(r.t_start, p->t_next - (p->D - 1)); s < p->t_next; ++s)
     CUDA_TRY(cudaMemcpyAsync(p->yhist + size_t(s % p->yh) * Fy, r.y + size_t(s % r.ring) * Fy, size_t(Fy) * 4,

@@ -384,7 +384,11 @@ struct PCursor {
   const int* tbl;           // per-layer block ranges of this CTA (PSmem::blk)
   int ti, s, st, blk, off;  // tick, stage, step, own block, chunk offset (tiles) in the block
   int b0, b1, len, nsteps, k, fstep;
+  int lim;  // last tick (launch-relative) the cursor may enter: a resident launch parks the
+            // cursor at the boundary of a tick the host has not requested (a CTA with no chunks
+            // would otherwise walk through every future tick)
   bool done;
+  __device__ __forceinline__ bool parked() const { return ti > lim; }
   const PLayer* L;
   __device__ __forceinline__ bool fwd() const { return st < k; }
   __device__ void begin_step(const PParams& P, const PStage* stages, const PLayer* layers) {
@@ -422,10 +426,11 @@ struct PCursor {
     begin_step(P, stages, layers);
   }
   __device__ void settle(const PParams& P, const PStage* stages, const PLayer* layers) {
-    while (!done && blk >= b1) next_step(P, stages, layers);
+    while (!done && !parked() && blk >= b1) next_step(P, stages, layers);
   }
   __device__ void init(const PParams& P, const PStage* stages, const PLayer* layers) {
     ti = s = st = fstep = 0;
+    lim = P.resident ? -1 : 0x7fffffff;
     done = P.n <= 0;
     if (done) return;
     begin_step(P, stages, layers);
@@ -462,7 +467,7 @@ __device__ void pn_producer(const PParams& P, const PLayer* layers, const PStage
   pf.init(P, stages, layers);
   uint32_t pf_idx = 0;
   auto top_up = [&]() {
-    while (!pf.done && pf_idx < chunk + uint32_t(P.pf_chunks)) {
+    while (!pf.done && !pf.parked() && pf_idx < chunk + uint32_t(P.pf_chunks)) {
       const long long t = pf.t(P);
       if (pf.fwd()) {
         prefetch_l2(pf.L->W[pn_fbuf(P, *pf.L, t)] + pf.foff(), uint32_t(pf.ntiles()) * PN_TILE * 4u);
@@ -475,15 +480,19 @@ __device__ void pn_producer(const PParams& P, const PLayer* layers, const PStage
   };
   top_up();
   int raw_ti = 0;  // backward loads of ticks <= raw_ti may start (every CTA finished tick ti-1)
-  int req_ti = -1;  // resident mode: ticks <= req_ti were requested by the host
   while (!cur.done && !dead) {
+    if (cur.parked()) {
+      // resident mode: no load of a tick the host has not requested (at a stop, nothing is in
+      // flight)
+      if (!pn_wait_request(P, cur.t(P), false)) break;
+      cur.lim = pf.lim = cur.ti;
+      cur.settle(P, stages, layers);
+      pf.settle(P, stages, layers);
+      top_up();
+      continue;
+    }
     const int ti = cur.ti;
     const long long t = cur.t(P);
-    if (P.resident && ti > req_ti) {
-      // no load of a tick the host has not requested: at a stop, nothing is in flight
-      if (!pn_wait_request(P, t, false)) break;
-      req_ti = ti;
-    }
     if (P.learn && ti > 0) {
       if (cur.fwd() && !cur.L->bw) {
         // forward-written layer: my consumers stored my rows at tick ti-1; fenced yet?
@@ -678,7 +687,7 @@ __device__ __forceinline__ const float* pn_target(const PParams& P, long long si
 
 // output row and loss partials of tick ti: per-run arrays, or two-tick rings (resident)
 __device__ __forceinline__ float* pn_outs(const PParams& P, int ti) {
-  return P.resident ? P.rout + size_t(ti & 1) * P.F : P.outs + size_t(ti) * P.F;
+  return P.resident ? P.rout + size_t((P.t0 + ti) & 1) * P.F : P.outs + size_t(ti) * P.F;  // host reads rout[t & 1]
 }
 __device__ __forceinline__ float* pn_lpart(const PParams& P, int ti) {
   return P.loss_part + size_t(P.resident ? (ti & 1) : ti) * P.G;
@@ -861,12 +870,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constan
         for (int j = bk0[4] + tid; j < bk0[5]; j += NCT) st_tv_gpu(xd + j, pack_tv(ld_volatile_f32(xr + j), tag_t));
       }
     }
-    // tick barrier. Learning: every CTA finished tick t-1 (orders this tick's weight stores
-    // after every read of their buffer, and keeps per-tick rings one tick deep). Inference:
-    // lagged by one tick (cache slots only).
+    // tick barrier: every CTA finished tick t-1. It orders this tick's weight stores after
+    // every read of their buffer (learning) and keeps the per-tick rings (cache slots mod 4,
+    // delta and input parities) at most one tick deep. The counter is cumulative, so only
+    // the full barrier bounds the skew: a lagged test (G * (t - 1) at tick t) can be met by
+    // the arrivals of CTAs running ahead while one CTA is several ticks behind (the jitter
+    // race detector stalled one CTA and the others overwrote cache slots it had not read).
     if (tid == 0) {
-      if (P.learn && t >= 1) pn_wait_cnt(P.tick_end, u64(G) * u64(t), P);
-      else if (!P.learn && t >= 2) pn_wait_cnt(P.tick_end, u64(G) * u64(t - 1), P);
+      if (t >= 1) pn_wait_cnt(P.tick_end, u64(G) * u64(t), P);
       __threadfence();
     }
     for (int s = 0; s < P.n_stages; ++s) {
