@@ -75,7 +75,7 @@ typedef struct pt_config {
   float lr;                          /* learning rate (SGD / Adam step size) */
   int32_t n_stages;                  /* D */
   const int32_t* stage_first_layer;  /* D+1 layer indices; [0] = 0, [D] = L (StagePlan) */
-  int32_t batch;                     /* M rows per tick (1..16) */
+  int32_t batch;                     /* M rows per tick (1..64) */
   int32_t learn;                     /* 1: forward+backward+update; 0: inference wave */
   int32_t act_delay;                 /* 1: SPEC reading (stages h<D backprop the previous tick's
                                         cache); 0: paper reading (current tick) */

@@ -429,7 +429,7 @@ int validate(const pt_config* c, std::string* why) {
   if (b[0] != 0 || b[D] != c->n_layers) return bad("stage plan must start at layer 0 and end at layer L");
   for (int h = 0; h < D; ++h)
     if (b[h] >= b[h + 1]) return bad("stage " + std::to_string(h + 1) + " is empty or out of order");
-  if (c->batch < 1 || c->batch > pt::MAXM) return bad("batch must be in [1, 16]");
+  if (c->batch < 1 || c->batch > pt::MAXM) return bad("batch must be in [1, " + std::to_string(pt::MAXM) + "]");
   for (int i = 0; i <= c->n_layers; ++i)
     if (pad_dim(c->dims[i]) > pt::MAX_LD)
       return bad("width " + std::to_string(c->dims[i]) + " exceeds the supported maximum 8192");

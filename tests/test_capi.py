@@ -43,7 +43,7 @@ def _cfg(dims, D_first, act=None, batch=1, **kw):
 @pytest.mark.parametrize("dims,sfl,kw,msg", [
     ([4, 4], [0, 1, 1], {}, "D=2 > L=1"),
     ([4, 4, 4, 4], [0, 2, 1, 3], {}, "empty or out of order"),
-    ([4, 4, 4], [0, 2], {"batch": 17}, "batch"),
+    ([4, 4, 4], [0, 2], {"batch": 65}, "batch"),
     ([4, 9000], [0, 1], {}, "8192"),
     ([4, 4], [1, 1], {}, "start at layer 0"),
     ([4, 4], [0, 1], {"act_delay": 2}, "act_delay"),

@@ -85,3 +85,33 @@ def test_drift2d_learning_curves_match_oracle():
         e_gpu = np.max(np.abs(g - o64) / o64)
         e_f32 = np.max(np.abs(o32 - o64) / o64)
         assert e_gpu <= max(4 * e_f32, 0.05), (counts, e_gpu, e_f32, g, o64, o32)
+
+
+def test_acceptance9_replay_window_trend(tmp_path):
+    """Acceptance #9: on a synthetic 10-class DatasetFile, held-out accuracy is
+    non-decreasing in the replay window W over {4, 16, 64} (§5.D, Fig. 4), for the
+    majority of 3 seeds. The loss averages over the window, so the trend is
+    flat-to-rising; a window counts as not worse within one point of accuracy. D = 2, the
+    window is the micro-batch of the B200 pipeline (generic path up to M = 64)."""
+    K, d, N = 10, 16, 1500
+    ok_seeds = 0
+    for seed in range(3):
+        rng = np.random.default_rng(seed)
+        mu = rng.standard_normal((K, d))
+        y = rng.integers(0, K, N + 2000)
+        x = mu[y] + rng.standard_normal((N + 2000, d))
+        path = str(tmp_path / f"train{seed}.ptds")
+        streams.dataset_write(path, x[:N].astype(np.float32), y[:N].astype(np.int32))
+        ds = streams.dataset_read(path)
+        acc = []
+        for W in (4, 16, 64):
+            xs, ys = streams.ReplayStream(ds, W).block(0, N)
+            m = mdl.mlp([d, 64, K], seed=seed, loss="softmax_ce")
+            p = engine.Pipeline(m, [2, 1], "sgd", 0.003, xs[0].astype(np.float32), ys[0].astype(np.float32))
+            p.run(xs.astype(np.float32), ys.astype(np.float32))
+            (W1, b1), (W2, b2) = p.get_layer(0), p.get_layer(1)
+            p.close()
+            h = np.maximum(x[N:] @ W1.T.astype(np.float64) + b1, 0.0)
+            acc.append(float(np.mean(np.argmax(h @ W2.T.astype(np.float64) + b2, axis=1) == y[N:])))
+        ok_seeds += all(acc[i + 1] >= acc[i] - 0.01 for i in range(2))
+    assert ok_seeds >= 2

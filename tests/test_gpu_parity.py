@@ -225,6 +225,13 @@ def test_c2_shape_short():
     _case([2048] * 33, [32, 31], 5, 1e-3)
 
 
+@pytest.mark.parametrize("M,opt,loss", [(32, "sgd", "mse"), (64, "sgd", "softmax_ce"), (64, "adam", "mse")])
+def test_microbatch_up_to_64(M, opt, loss):
+    """Micro-batches above 16 (replay windows W in {4, 16, 64}) on the generic
+    tick-kernel path."""
+    _case([40, 96, 72, 24], [2, 3], 14, 0.02 if opt == "sgd" else 1e-3, M=M, optimizer=opt, loss=loss)
+
+
 def test_microbatch_16():
     """M=16 replay window (config 4 semantics) on the generic path."""
     _case([64, 256, 128, 32], [2, 3], 12, 0.02, M=16)
