@@ -70,11 +70,13 @@ def plan_counts(L, D):
     return counts
 
 
-def algorithmic_bytes_per_tick(widths, learn=True):
-    """learn Σ(12·n_in·n_out + 4·n_out), infer Σ 4·n_in·n_out (fp32)."""
+def algorithmic_bytes_per_tick(widths, learn=True, optimizer="sgd"):
+    """learn Σ(12·n_in·n_out + 4·n_out), infer Σ 4·n_in·n_out (fp32). Adam reads
+    and writes its two moments too: Σ(28·n_in·n_out + 20·n_out) (optimizer row)."""
+    w_b, b_b = (28, 20) if optimizer == "adam" else (12, 4)
     tot = 0
     for i in range(len(widths) - 1):
-        tot += (12 if learn else 4) * widths[i] * widths[i + 1] + (4 * widths[i + 1] if learn else 0)
+        tot += (w_b if learn else 4) * widths[i] * widths[i + 1] + (b_b * widths[i + 1] if learn else 0)
     return tot
 
 
@@ -212,28 +214,34 @@ def extra_configs(peak):
     import torch
     from paper_2210_09147_b200 import engine, model as mdl, streams
     c5 = [1024, 2048, 4096, 8192, 8192, 4096, 2048, 1024] * 3 + [1024]
-    cases = [("C3", "64-layer 4096-wide MLP inference wave, D=8 stages on 1 GPU", [4096] * 65, 8, False, 1, 8),
-             ("C4", "32-layer 4096-wide MLP, micro-batch 16, D=8 stages on 1 GPU", [4096] * 33, 8, True, 16, 8),
-             ("C5", "uneven widths 1024..8192 (24 layers), D=8 stages on 1 GPU", c5, 8, True, 1, 16)]
+    cases = [("C3", "64-layer 4096-wide MLP inference wave, D=8 stages on 1 GPU", [4096] * 65, 8, False, 1, 8,
+              "sgd", "mse"),
+             ("C4", "32-layer 4096-wide MLP, micro-batch 16, D=8 stages on 1 GPU", [4096] * 33, 8, True, 16, 8,
+              "sgd", "mse"),
+             ("C4_adam_ce", "C4 with Adam and softmax-CE (PAPER.md:863 replay batches use Adam), D=8 on 1 GPU",
+              [4096] * 33, 8, True, 16, 8, "adam", "softmax_ce"),
+             ("C5", "uneven widths 1024..8192 (24 layers), D=8 stages on 1 GPU", c5, 8, True, 1, 16, "sgd", "mse")]
     res = {}
-    for name, desc, widths, D, learn, M, ticks in cases:
+    for name, desc, widths, D, learn, M, ticks, opt, loss in cases:
         try:
-            m = mdl.mlp(widths, seed=0, dtype=np.float32)
+            m = mdl.mlp(widths, seed=0, dtype=np.float32, loss=loss)
             st = streams.SmoothStream(widths[0], widths[-1], seed=1, batch=M)
             xs, ys = st.block(0, ticks)
+            if loss == "softmax_ce":
+                ys = np.argmax(ys, axis=-1).astype(np.float32)
             xs = torch.tensor(xs, dtype=torch.float32, device="cuda")
             ys = torch.tensor(ys, dtype=torch.float32, device="cuda")
             x0 = xs[0].cpu().numpy() if M > 1 else xs[0, 0].cpu().numpy()
             y0 = ys[0].cpu().numpy() if M > 1 else ys[0, 0].cpu().numpy()
-            p = engine.Pipeline(m, balanced_counts(widths, D, learn), "sgd", 1e-3 if learn else 0.0, x0, y0,
-                                learn=learn)
+            p = engine.Pipeline(m, balanced_counts(widths, D, learn), opt, (1e-3 if opt == "sgd" else 1e-4)
+                                if learn else 0.0, x0, y0, learn=learn)
             best = 1e30
             for _ in range(3):
                 p.run(xs, ys)
                 p.sync()
                 best = min(best, p.last_kernel_ms())
             us = best * 1e3 / ticks
-            byt = algorithmic_bytes_per_tick(widths, learn)
+            byt = algorithmic_bytes_per_tick(widths, learn, opt)
             res[name] = {"workload": desc, "kernel": KERNEL_NAMES[p.kernel_path], "tick_us": round(us, 1), "samples_per_s": round(M * 1e6 / us, 1),
                          "achieved_gbs": round(byt / (us * 1e-6) / 1e9, 1),
                          "frac_of_hbm_roofline": round(byt / (us * 1e-6) / 1e9 / peak, 4)}

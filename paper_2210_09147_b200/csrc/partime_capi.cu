@@ -231,6 +231,7 @@ struct pt_pipeline {
   int t_smem = 0, t_maxn = 0;
   float* t_part = nullptr;
   float* t_delta = nullptr;
+  float* t_ce = nullptr;  // softmax-CE partials of the tile path [G][M][2]
   u64* t_bars = nullptr;  // [0] grid barrier, [16] weight write-back counter
   CUtensorMap* d_tmaps = nullptr;
   pt::TLayer* d_tlayers = nullptr;
@@ -580,6 +581,7 @@ int setup_tile(pt_pipeline* p) {
   PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&p->t_part), size_t(pt::T_Q) * M * maxn * 4));
   PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&p->t_delta), size_t(M) * maxn * 4));
   PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&p->t_bars), 32 * sizeof(u64)));
+  PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&p->t_ce), size_t(p->G) * M * 2 * 4));
   std::vector<CUtensorMap> maps(2 * p->layers.size());
   std::vector<pt::TLayer> tl(p->layers.size());
   PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&p->d_tmaps), maps.size() * sizeof(CUtensorMap)));
@@ -592,6 +594,11 @@ int setup_tile(pt_pipeline* p) {
     tl[i].tmf = p->d_tmaps + 2 * i;
     tl[i].tmb = p->d_tmaps + 2 * i + 1;
     tl[i].b = Lh.b;
+    tl[i].mW = Lh.mW;
+    tl[i].vW = Lh.vW;
+    tl[i].mb = Lh.mb;
+    tl[i].vb = Lh.vb;
+    tl[i].ld = Lh.ld_in;
     tl[i].n_in = Lh.n_in;
     tl[i].n_out = Lh.n_out;
     tl[i].act = Lh.act;
@@ -628,7 +635,8 @@ int setup_tile(pt_pipeline* p) {
   p->t_smem = 1024 + pt::T_NSLOT * pt::T_SLOT_FLOATS * 4 + pt::T_NB * 2 * M * pt::T_CK * 4 + pt::T_NB * 2 * pt::T_CK * pt::T_MAXM * 4 + 2 * 128 * pt::T_MAXM * 4 + 64 +
               (3 * pt::T_NSLOT + 5 * pt::T_NB + 4) * 8 + 16;
   if (p->t_smem > pt::SMEM_MAX) return fail(PT_EINVAL, "tile path shared-memory plan exceeds 227 KB");
-  CUDA_TRY(cudaFuncSetAttribute(pt::tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, p->t_smem));
+  CUDA_TRY(cudaFuncSetAttribute(pt::tile_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, p->t_smem));
+  CUDA_TRY(cudaFuncSetAttribute(pt::tile_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, p->t_smem));
   return PT_OK;
 }
 
@@ -863,7 +871,8 @@ int create_impl(const pt_config* c, pt_pipeline* p) {
     // first launch of a kernel may wait for the kernels running on the device; a persistent
     // stage kernel waiting for a neighbour (another handle, part or process) that is itself
     // blocked in such a load would only end at the watchdog.
-    const void* others[] = {(const void*)pt::panel_kernel<0>, (const void*)pt::tile_kernel,
+    const void* others[] = {(const void*)pt::panel_kernel<0>, (const void*)pt::tile_kernel<0>,
+                            (const void*)pt::tile_kernel<1>,
                             (const void*)pt::epilogue_kernel, (const void*)pt::pn_to_tiles,
                             (const void*)pt::pn_from_tiles};
     cudaFuncAttributes fa;
@@ -877,7 +886,7 @@ int create_impl(const pt_config* c, pt_pipeline* p) {
   if (p->G > sms * per_sm) return fail(PT_EINVAL, "grid exceeds co-resident CTA capacity");
   {
     // micro-batch tensor-core path: every width a multiple of 256, M == 16, all stages here
-    bool ok = p->M == 16 && p->opt == PT_OPT_SGD && p->loss == PT_LOSS_MSE;
+    bool ok = p->M == 16;  // SGD or Adam, MSE or softmax-CE
     int units = 0;
     for (int i = 0; i <= p->L && ok; ++i) ok = (p->dims[i] % 256) == 0;
     for (int i = 0; i < p->L && ok; ++i) units = std::max(units, std::max(p->dims[i + 1], p->dims[i]) / 128 * pt::T_Q);
@@ -1507,6 +1516,18 @@ int run_impl(pt_pipeline* p, const float* xs, const float* ys, int64_t n, float*
     T.F = F;
     T.G = p->G;
     T.lr = p->lr;
+    T.opt = p->opt;
+    T.loss = p->loss;
+    T.Fy = Fy;
+    T.b1 = P.b1;
+    T.b2 = P.b2;
+    T.b1d = P.b1d;
+    T.b2d = P.b2d;
+    T.omb1 = P.omb1;
+    T.omb2 = P.omb2;
+    T.eps = P.eps;
+    T.ce = p->t_ce;
+    T.bad_target = p->d_bad_target;
     T.xs = p->xs_pad;
     T.ldx = ld0;
     T.ys = ys_dev;
@@ -1533,7 +1554,7 @@ int run_impl(pt_pipeline* p, const float* xs, const float* ys, int64_t n, float*
     CUDA_TRY(cudaMemsetAsync(p->t_bars, 0, 32 * sizeof(u64), p->stream));
     void* targs[] = {&T};
     CUDA_TRY(cudaEventRecord(p->ev0, p->stream));
-    CUDA_TRY(cudaLaunchCooperativeKernel((const void*)pt::tile_kernel, dim3(p->G), dim3(pt::T_THREADS), targs,
+    CUDA_TRY(cudaLaunchCooperativeKernel(p->opt == PT_OPT_ADAM ? (const void*)pt::tile_kernel<1> : (const void*)pt::tile_kernel<0>, dim3(p->G), dim3(pt::T_THREADS), targs,
                                          size_t(p->t_smem), p->stream));
     CUDA_TRY(cudaEventRecord(p->ev1, p->stream));
   } else {

@@ -53,6 +53,8 @@ struct TLayer {
   const CUtensorMap* tmf;  // box [128 rows][32 cols], SWIZZLE_128B
   const CUtensorMap* tmb;  // box [64 rows][32 cols], SWIZZLE_128B_ATOM_32B
   float* b;
+  float *mW, *vW, *mb, *vb;  // Adam moments (row-major like W, row pitch ld); null for SGD
+  int ld;
   int n_in, n_out, act;
   int a_in, a_out;  // offsets (floats) of a_i, a_{i+1} in a stage cache slot ([M][n] each)
 };
@@ -82,6 +84,11 @@ struct TParams {
   const TLayer* layers;
   int n_stages, M, D, learn, act_delay, F, G;
   float lr;
+  int opt, loss, Fy;         // optimizer (0 SGD, 1 Adam), loss (0 MSE, 1 softmax-CE), target width
+  float b1, b2, eps, omb1, omb2;  // Adam, as in pt::Params
+  double b1d, b2d;
+  float* ce;                 // softmax-CE: per-CTA (max, sum exp) partials [G][M][2]
+  long long* bad_target;     // first sample whose class index is not in [0, F)
   const float* xs;  // [n][M][ldx]
   int ldx;
   const float* ys;  // [n][M][F]
@@ -507,7 +514,16 @@ __device__ __forceinline__ void t_lo_pass_b(const float* tile, uint32_t lo_tmem)
 // In-place SGD step on a B chunk once all its MMAs are done (group B): the tensor core has
 // computed D[c][r] = sum_m a[m][c] delta[m][r] (3xTF32, columns [0,64) hi*hi + lo*hi,
 // [64,128) hi*lo); thread = column c (its TMEM lane), 64 rows: w' = w - lr * (d0 + d1).
-__device__ __forceinline__ void t_apply_update(float* tile, uint32_t upd_tmem, float nlr) {
+// Adam step on one weight (the same arithmetic as pt::adam1)
+__device__ __forceinline__ float t_adam1(float w, float g, float& m, float& v, const TParams& P, float c1, float c2) {
+  m = fmaf(P.b1, m, P.omb1 * g);
+  v = fmaf(P.b2, v, P.omb2 * g * g);
+  return w - P.lr * (m * c1) / (sqrtf(v * c2) + P.eps);
+}
+
+template <bool ADAM>
+__device__ __forceinline__ void t_apply_update(float* tile, uint32_t upd_tmem, float nlr, const TParams& P,
+                                               float* mrow, float* vrow, int ld, float c1, float c2) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cl = 32 * (warp & 3) + lane;
   float* colp[4];
@@ -523,12 +539,94 @@ __device__ __forceinline__ void t_apply_update(float* tile, uint32_t upd_tmem, f
     float w[T_UPR];
 #pragma unroll
     for (int rr = 0; rr < T_UPR; ++rr) w[rr] = colp[rr & 3][(rh * T_UPR + rr - (rr & 3)) * 32];
+    if (ADAM) {
+      // Adam: the moments of (row 32 rh + rr, column cl), coalesced across the warp's columns;
+      // 16 rows in flight at a time (register budget)
+      float g[T_UPR];
 #pragma unroll
-    for (int rr = 0; rr < T_UPR; ++rr)
-      colp[rr & 3][(rh * T_UPR + rr - (rr & 3)) * 32] = fmaf(nlr, d0[rr] + d1[rr], w[rr]);
+      for (int rr = 0; rr < T_UPR; ++rr) g[rr] = d0[rr] + d1[rr];
+#pragma unroll
+      for (int r0 = 0; r0 < T_UPR; r0 += 16) {
+        float mm[16], vv[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          mm[q] = __ldcg(mrow + size_t(rh * T_UPR + r0 + q) * ld + cl);
+          vv[q] = __ldcg(vrow + size_t(rh * T_UPR + r0 + q) * ld + cl);
+        }
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const int rr = r0 + q;
+          colp[rr & 3][(rh * T_UPR + rr - (rr & 3)) * 32] = t_adam1(w[rr], g[rr], mm[q], vv[q], P, c1, c2);
+          __stcg(mrow + size_t(rh * T_UPR + rr) * ld + cl, mm[q]);
+          __stcg(vrow + size_t(rh * T_UPR + rr) * ld + cl, vv[q]);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int rr = 0; rr < T_UPR; ++rr)
+        colp[rr & 3][(rh * T_UPR + rr - (rr & 3)) * 32] = fmaf(nlr, d0[rr] + d1[rr], w[rr]);
+    }
   }
 }
 
+// Softmax cross-entropy at the network's output (the tick kernel's formula):
+// delta[m][r] = (softmax(z_m)[r] - onehot(y_m)[r]) / M * act'(a), loss = sum_m (lse_m - z_m[y_m])
+// (the epilogue divides by M). The outputs of every CTA are in the stage cache once the first
+// grid barrier passes; each CTA reduces (max, sum exp) over its slice of rows per sample, and
+// after the second barrier every CTA combines the G partials in the same fixed order.
+__device__ __noinline__ void t_softmax_ce(const TParams& P, const TLayer& L, const float* Ccur, const float* y, long long sid, int ti,
+                             u64& gen, int gtid, int gthreads, int st_id, float* s_lse) {
+  const int M = P.M, G = P.G, c = blockIdx.x, n = L.n_out;
+  const float* z = Ccur + L.a_out;  // [M][n]
+  t_grid_sync(P, gen);
+  const int per = (n + G - 1) / G, r0 = min(n, c * per), r1 = min(n, r0 + per);
+  if (st_id < M) {
+    const int m = st_id;
+    float mx = -INFINITY;
+    for (int r = r0; r < r1; ++r) mx = fmaxf(mx, t_ld(z + size_t(m) * n + r));
+    float se = 0.f;
+    if (r1 > r0)
+      for (int r = r0; r < r1; ++r) se += expf(t_ld(z + size_t(m) * n + r) - mx);
+    P.ce[(size_t(c) * M + m) * 2] = mx;
+    P.ce[(size_t(c) * M + m) * 2 + 1] = se;
+  }
+  t_grid_sync(P, gen);
+  if (st_id < M) {
+    const int m = st_id;
+    float mx = -INFINITY;
+    for (int k = 0; k < G; ++k) mx = fmaxf(mx, t_ld(P.ce + (size_t(k) * M + m) * 2));
+    float se = 0.f;
+    for (int k = 0; k < G; ++k) {
+      const float pm = t_ld(P.ce + (size_t(k) * M + m) * 2), ps = t_ld(P.ce + (size_t(k) * M + m) * 2 + 1);
+      if (ps > 0.f) se += ps * expf(pm - mx);
+    }
+    s_lse[m] = mx + logf(se);
+  }
+  simt_sync();
+  float lsum = 0.f;
+  for (int e = gtid; e < M * n; e += gthreads) {
+    const int m = e / n, r = e - m * n;
+    const float a = t_ld(z + size_t(m) * n + r);
+    const int tgt = y ? int(y[m]) : -1;
+    const float g = y ? (expf(a - s_lse[m]) - (r == tgt ? 1.f : 0.f)) / float(M) : 0.f;
+    if (P.learn) P.delta[size_t(m) * P.max_n + r] = g * dact_fn(L.act, a);
+  }
+  if (c == 0 && st_id == 0) {
+    for (int m = 0; m < M && y; ++m) {
+      const int tgt = int(y[m]);
+      if (!(y[m] >= 0.f && y[m] < float(P.F) && float(tgt) == y[m])) {
+        atomicMin(P.bad_target, sid);
+        continue;
+      }
+      lsum += s_lse[m] - t_ld(z + size_t(m) * n + tgt);
+    }
+  }
+  if (st_id == 0) P.loss_part[size_t(ti) * G + c] = (c == 0) ? lsum : 0.f;
+}
+
+// OPT: 0 SGD, 1 Adam (separate instantiations: the Adam moments' registers stay out of the
+// SGD kernel)
+template <int OPT>
 __global__ void __launch_bounds__(T_THREADS, 1) tile_kernel(const __grid_constant__ TParams P) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1024-B alignment of the swizzled tiles
@@ -603,6 +701,14 @@ __global__ void __launch_bounds__(T_THREADS, 1) tile_kernel(const __grid_constan
         const int h = S.h;
         const bool is_last = (h == P.D);
         const bool upd = t_upd(P, t, h);
+        // Adam bias corrections of this stage's k-th update (k counts from the warm-up gate;
+        // in double, as pt::tick_kernel)
+        float c1 = 1.f, c2 = 1.f;
+        if (OPT == 1 && upd) {
+          const double k = double(t - (2LL * P.D - h - 1) + 1);
+          c1 = float(1.0 / (1.0 - pow(P.b1d, k)));
+          c2 = float(1.0 / (1.0 - pow(P.b2d, k)));
+        }
         float* Ccur = S.cache[cur];
         const float* Cb = (h < P.D && P.act_delay) ? S.cache[prv] : S.cache[cur];  // backward cache
         // stage input: x_t (h = 1) or inslot[(t-1) % 2]
@@ -639,7 +745,14 @@ __global__ void __launch_bounds__(T_THREADS, 1) tile_kernel(const __grid_constan
               float sd = 0.f;
 #pragma unroll
               for (int m = 0; m < T_MAXM; ++m) sd += dv[m];
-              L.b[r] = fmaf(nlr, sd, t_ld(L.b + r));
+              if (OPT == 1) {
+                float mm = t_ld(L.mb + r), vv = t_ld(L.vb + r);
+                L.b[r] = t_adam1(t_ld(L.b + r), sd, mm, vv, P, c1, c2);
+                L.mb[r] = mm;
+                L.vb[r] = vv;
+              } else {
+                L.b[r] = fmaf(nlr, sd, t_ld(L.b + r));
+              }
             }
           }
           t_trace(P, tr, 1);
@@ -713,14 +826,17 @@ __global__ void __launch_bounds__(T_THREADS, 1) tile_kernel(const __grid_constan
               }
               TOpnd op;
               op.fetch(osrc, old, M);
-              auto apply = [&](uint32_t jj, uint32_t bb) {
+              auto apply = [&](uint32_t jj, uint32_t bb, int chn) {
                 // chunk jj: all its MMAs are done -> SGD step in place -> producer stores the tile
                 const int pslot = jj % T_NSLOT;
                 t_wait(&sm.mdone[jj % T_NB], (jj / T_NB) & 1, P);
                 tc_fence_after();
                 t_trace(P, tr, 9);
                 if (upd) {
-                  t_apply_update(sm.ring + size_t(pslot) * T_SLOT_FLOATS, tbase + T_UPD_COL + (bb & 1) * 128, nlr);
+                  // Adam: this chunk's rows r0.. and the unit's 128 columns c0.. of the moments
+                  const size_t mo = size_t(q * (L.n_out / T_Q) + chn * T_CK) * L.ld + size_t(blk) * 128;
+                  t_apply_update<OPT == 1>(sm.ring + size_t(pslot) * T_SLOT_FLOATS, tbase + T_UPD_COL + (bb & 1) * 128, nlr, P,
+                                 OPT == 1 ? L.mW + mo : nullptr, OPT == 1 ? L.vW + mo : nullptr, L.ld, c1, c2);
                   fence_proxy_async_shared();  // W' -> the producer's TMA store
                 }
                 tc_fence_before();
@@ -755,12 +871,12 @@ __global__ void __launch_bounds__(T_THREADS, 1) tile_kernel(const __grid_constan
                 }
                 if (sp.fwd) ++fj;
                 if (!sp.fwd) {
-                  if (ch > 0) apply(j - 1, bj);
+                  if (ch > 0) apply(j - 1, bj, ch - 1);
                   if (ch > 0) ++bj;
                 }
               }
               if (!sp.fwd) {
-                apply(j - 1, bj);
+                apply(j - 1, bj, sp.nchunks - 1);
                 ++bj;
               }
             }
@@ -789,9 +905,10 @@ __global__ void __launch_bounds__(T_THREADS, 1) tile_kernel(const __grid_constan
             const long long sid = t - (P.D - 1);
             const float* y = nullptr;
             if (last_of_net && sid >= 0) {
-              if (sid >= P.t0) y = P.ys ? P.ys + size_t(sid - P.t0) * M * P.F : nullptr;
-              else if (P.yhist) y = P.yhist + size_t(sid % P.yh) * M * P.F;
+              if (sid >= P.t0) y = P.ys ? P.ys + size_t(sid - P.t0) * M * P.Fy : nullptr;
+              else if (P.yhist) y = P.yhist + size_t(sid % P.yh) * M * P.Fy;
             }
+            const bool ce = last_of_net && P.loss == 1;
             float lacc = 0.f;
             const int n = L.n_out;
             for (int e = gtid; e < M * n; e += gthreads) {
@@ -803,7 +920,9 @@ __global__ void __launch_bounds__(T_THREADS, 1) tile_kernel(const __grid_constan
               const float a = act_fn(L.act, z);
               Ccur[L.a_out + size_t(m) * n + r] = a;
               if (last_layer && h < P.D) S.down_inslot[cur][size_t(m) * n + r] = a;
-              if (last_of_net) {
+              if (ce) {
+                P.outs[(size_t(ti) * M + m) * P.F + r] = a;  // softmax-CE: delta and loss below
+              } else if (last_of_net) {
                 P.outs[(size_t(ti) * M + m) * P.F + r] = a;
                 float g = 0.f;
                 if (y) {
@@ -818,7 +937,8 @@ __global__ void __launch_bounds__(T_THREADS, 1) tile_kernel(const __grid_constan
                 P.delta[size_t(m) * P.max_n + r] = t_ld(S.gslot[prv] + size_t(m) * n + r) * dact_fn(L.act, ao);
               }
             }
-            if (last_of_net) {
+            if (ce) t_softmax_ce(P, L, Ccur, y, sid, ti, gen, gtid, gthreads, st_id, sm.red);
+            if (last_of_net && !ce) {
               // fixed-order CTA sum of the loss partials
               float v = warp_sum(lacc);
               if (lane == 0) sm.red[warp - 2] = v;

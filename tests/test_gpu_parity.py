@@ -327,6 +327,20 @@ def test_tile_small(D):
     _tile_case([256, 512, 256, 256], counts, 12, 0.02)
 
 
+@pytest.mark.parametrize("opt,loss,D", [("adam", "mse", 1), ("sgd", "softmax_ce", 2), ("adam", "softmax_ce", 2)])
+def test_tile_adam_softmax_ce(opt, loss, D):
+    """Adam and softmax-CE on the tcgen05 tile kernel (PAPER.md:863 runs
+    the replay-batch experiment with Adam)."""
+    widths, counts = [256, 512, 256, 256], {1: [5], 2: [2, 3]}[D]
+    m, st, mk = _pipe(widths, counts, 0.01, M=16)
+    xs, ys = st.block(0, 2)
+    p = engine.Pipeline(mdl.mlp(widths, seed=0, loss=loss), counts, opt, 1e-3,
+                        xs[0], ys[0] if loss == "mse" else np.zeros(16, np.float32))
+    assert p.kernel_path == "tile"
+    p.close()
+    _tile_case(widths, counts, 12, 1e-3 if opt == "adam" else 0.02, optimizer=opt, loss=loss)
+
+
 @pytest.mark.parametrize("act_delay", [0, 1])
 def test_tile_act_delay_tanh(act_delay):
     _tile_case([256, 256, 512, 256], [2, 3], 10, 0.02, act="tanh", act_delay=act_delay)

@@ -53,6 +53,18 @@ def test_c4_tile_d8():
     _case(w, counts, 8, 1e-3, M=16)
 
 
+def test_c4_tile_d8_adam_ce():
+    """Config 4's shape with Adam and softmax-CE on the tile kernel (a bench other_configs line)."""
+    from paper_2210_09147_b200 import engine, model as mdl
+    w = [4096] * 33
+    counts = _bench_counts(w, 8, True)
+    p = engine.Pipeline(mdl.mlp(w, seed=0, loss="softmax_ce"), counts, "adam", 1e-4,
+                        np.zeros((16, 4096), np.float32), np.zeros(16, np.float32))
+    assert p.kernel_path == "tile"
+    p.close()
+    _case(w, counts, 6, 1e-4, M=16, optimizer="adam", loss="softmax_ce")
+
+
 def test_c5_uneven_d8():
     """Config 5: uneven widths 1024..8192, DP-balanced stages, D = 8, 8 ticks."""
     _case(C5, _bench_counts(C5, 8, True), 8, 1e-3)
