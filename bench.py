@@ -405,6 +405,8 @@ def main():
     if world > 1:
         per_rank = [None] * world
         dist.all_gather_object(per_rank, mine, group=gloo)
+    kpath = pipe.kernel_path
+    pipe.close()  # ends the per-sample API's resident launch before other pipelines run
     h2d = T * BATCH * (widths[0] + widths[-1]) * 4
     d2h = T * BATCH * widths[-1] * 4 + T * 4 + T
 
@@ -419,7 +421,6 @@ def main():
             peak, peak_src = float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
         peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
-    kpath = pipe.kernel_path
     tpt, ncu = load_traffic(kpath)
     if ncu is None or ncu.get("config") != {"width": args.width, "layers": args.layers, "stages": D}:
         tpt = None  # the committed capture is for another workload

@@ -10,7 +10,9 @@
 #include <cuda_runtime.h>
 #include <unistd.h>
 
+#include <algorithm>
 #include <atomic>
+#include <mutex>
 #include <chrono>
 #include <thread>
 #include <cmath>
@@ -1173,6 +1175,48 @@ void panel_common(pt_pipeline* p, pt::PParams& Q) {
 // without a launch per sample: PAPER.md:600-605 removed the per-tick enqueue cost with CUDA
 // Graphs; here one persistent panel-kernel launch serves consecutive pt_step calls (see
 // PParams::resident in pt_panel.cuh). Any other entry point stops it first (resident_stop).
+// A resident launch holds its SMs until the host posts a stop. Another handle's cooperative
+// launch on the same device could then never become co-resident, so every launch first stops
+// the resident launches of the other handles on its device (process-wide registry).
+std::mutex g_res_mu;
+std::vector<pt_pipeline*> g_resident;
+int resident_stop(pt_pipeline* p);
+
+void resident_register(pt_pipeline* p, bool on) {
+  std::lock_guard<std::mutex> lk(g_res_mu);
+  auto it = std::find(g_resident.begin(), g_resident.end(), p);
+  if (on && it == g_resident.end()) g_resident.push_back(p);
+  if (!on && it != g_resident.end()) g_resident.erase(it);
+}
+
+int stop_foreign_residents(pt_pipeline* self) {
+  std::vector<pt_pipeline*> others;
+  {
+    std::lock_guard<std::mutex> lk(g_res_mu);
+    for (pt_pipeline* q : g_resident)
+      if (q != self && q->device == self->device) others.push_back(q);
+  }
+  for (pt_pipeline* q : others) {
+    // the owner may be inside a step of its own: wait for the handle (single driver)
+    const auto t_begin = std::chrono::steady_clock::now();
+    int z = 0;
+    while (!q->busy.compare_exchange_strong(z, 1)) {
+      z = 0;
+      if (std::chrono::steady_clock::now() - t_begin > std::chrono::nanoseconds(self->timeout_ns))
+        return fail(PT_EBUSY, "another pipeline's resident pt_step launch holds the device");
+      std::this_thread::yield();
+    }
+    int r;
+    {
+      DevGuard dg(q->device);
+      r = resident_stop(q);
+    }
+    q->busy.store(0);
+    if (r != PT_OK) return r;
+  }
+  return PT_OK;
+}
+
 bool resident_eligible(const pt_pipeline* p) {
   if (!p->panel || p->group() || !p->has_first() || !p->has_last() || p->M != 1) return false;
   const char* e = getenv("PT_RESIDENT");
@@ -1214,6 +1258,7 @@ T* to_dev(const pt_pipeline* p, T* hptr) {
 
 int resident_start(pt_pipeline* p) {
   PT_TRY(check_ready(p));
+  PT_TRY(stop_foreign_residents(p));
   PT_TRY(resident_alloc(p));
   if (p->legacy_dirty) {
     CUDA_TRY(cudaStreamSynchronize(0));
@@ -1244,6 +1289,7 @@ int resident_start(pt_pipeline* p) {
                                        size_t(p->pn_smem), p->stream));
   r.on = true;
   r.t_start = p->t_next;
+  resident_register(p, true);
   return PT_OK;
 }
 
@@ -1252,6 +1298,7 @@ int resident_start(pt_pipeline* p) {
 int resident_stop(pt_pipeline* p) {
   pt_pipeline::Resident& r = p->res;
   if (!r.on) return PT_OK;
+  resident_register(p, false);
   std::atomic_thread_fence(std::memory_order_seq_cst);
   *reinterpret_cast<volatile long long*>(r.req) = pt::PN_STOP;
   std::atomic_thread_fence(std::memory_order_seq_cst);
@@ -1303,6 +1350,7 @@ int resident_step(pt_pipeline* p, const float* x, const float* y, float* out, fl
       const cudaError_t q = cudaStreamQuery(p->stream);
       if (q != cudaErrorNotReady) {  // the launch ended without completing the step
         r.on = false;
+        resident_register(p, false);
         if (q != cudaSuccess) return fail(PT_ECUDA, std::string("resident launch failed: ") + cudaGetErrorString(q));
         PT_TRY(read_status(p));
         return fail(PT_ESTATE, "resident launch ended before completing step " + std::to_string(t));
@@ -1334,6 +1382,7 @@ int resident_step(pt_pipeline* p, const float* x, const float* y, float* out, fl
 int run_impl(pt_pipeline* p, const float* xs, const float* ys, int64_t n, float* outs, float* losses,
              uint8_t* valid, int where, bool wait = true) {
   PT_TRY(check_ready(p));
+  PT_TRY(stop_foreign_residents(p));
   if (p->pend.active) return fail(PT_EBUSY, "contract violation: previous run not finished (pt_sync)");
   if (n <= 0) return PT_OK;
   if (p->legacy_dirty) {

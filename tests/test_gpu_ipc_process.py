@@ -24,7 +24,7 @@ CASES = {"panel": ([32, 64, 64, 64, 16], [4, 3], 12, 1),
 
 def _data(case):
     from paper_2210_09147_b200 import streams
-    widths, counts, T, M = CASES[case]
+    widths, counts, T, M = CASES[case.replace("_2gpu", "")]
     st = streams.SmoothStream(widths[0], widths[-1], seed=5, batch=M)
     xs, ys = st.block(0, T)
     return widths, counts, T, M, xs.astype(np.float32), ys.astype(np.float32)
@@ -42,7 +42,8 @@ def _worker(rank, port, q, case):
     import torch.distributed as dist
     from paper_2210_09147_b200 import dist as pdist, model as mdl
     dist.init_process_group("gloo", rank=rank, world_size=2)
-    torch.cuda.set_device(0)
+    # "_2gpu" cases: one GPU per process (NVLink peer stores through CUDA IPC), else both on GPU 0
+    torch.cuda.set_device(rank if case.endswith("_2gpu") else 0)
     widths, counts, T, M, xs, ys = _data(case)
     pipe = pdist.build_distributed(mdl.mlp(widths, seed=4), counts, "sgd", 0.05, _sample(xs, M), _sample(ys, M),
                                    timeout_ms=60000)
@@ -59,10 +60,14 @@ def _worker(rank, port, q, case):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("case", list(CASES))
+@pytest.mark.parametrize("case", list(CASES) + [pytest.param("panel_2gpu", marks=pytest.mark.gpu2),
+                                                pytest.param("tile_2gpu", marks=pytest.mark.gpu2)])
 def test_two_process_ipc_matches_single_process(case):
+    import torch
     import torch.multiprocessing as mp
     from paper_2210_09147_b200 import engine, model as mdl
+    if case.endswith("_2gpu") and torch.cuda.device_count() < 2:
+        pytest.skip("needs two visible GPUs")
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]

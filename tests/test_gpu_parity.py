@@ -166,6 +166,26 @@ def test_resident_steps_interleaved_with_runs(loss):
     b.close()
 
 
+def test_resident_launch_yields_to_other_pipelines():
+    """A resident pt_step launch holds its SMs; another pipeline's run on the same device stops
+    it first (and the first pipeline's next step restarts it), with results unchanged."""
+    widths, counts, T = [64, 96, 96, 32], [2, 3], 12
+    m = mdl.mlp(widths, seed=3)
+    xs, ys = streams.SmoothStream(widths[0], widths[-1], seed=4).block(0, T)
+    xs, ys = xs.astype(np.float32), ys.astype(np.float32)
+    mk = lambda: engine.Pipeline(m, counts, "sgd", 0.05, xs[0, 0], ys[0, 0])
+    a, b, ref = mk(), mk(), mk()
+    o_ref, _, _ = ref.run(xs, ys)
+    outs = []
+    for t in range(T):
+        outs.append(a.step(xs[t, 0], ys[t, 0]).output)   # resident launch of `a`
+        o_b, _, _ = b.run(xs[t:t + 1], ys[t:t + 1])        # stops it, runs, `a` restarts next
+        assert np.array_equal(o_b[0, 0], o_ref[t, 0])
+    assert np.array_equal(np.array(outs), o_ref[:, 0])
+    for p in (a, b, ref):
+        p.close()
+
+
 def test_resident_step_errors():
     """The resident path reports a non-finite loss with its step and a softmax-CE
     target outside [0, F), like pt_run."""
