@@ -268,6 +268,8 @@ struct pt_pipeline {
     int* flag = nullptr;
     float *x = nullptr, *y = nullptr, *out = nullptr;
     u64* xin = nullptr;
+    u64* ytag = nullptr;  // tagged device targets [ring][ldy]
+    int ldy = 0;
     long long* relay = nullptr;
     float* lpart = nullptr;
   } res;
@@ -1246,6 +1248,8 @@ int resident_alloc(pt_pipeline* p) {
   CUDA_TRY(cudaHostGetDevicePointer(&dh, r.host, 0));
   r.dev_off = static_cast<char*>(dh) - static_cast<char*>(r.host);
   PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&r.xin), size_t(2) * r.ldx * sizeof(u64)));
+  r.ldy = (p->F() + pt::PN_TS - 1) / pt::PN_TS * pt::PN_TS;  // the loss gather's row length
+  PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&r.ytag), size_t(r.ring) * r.ldy * sizeof(u64)));
   PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&r.relay), 64));
   PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&r.lpart), size_t(2) * p->G * sizeof(float)));
   return PT_OK;
@@ -1281,6 +1285,8 @@ int resident_start(pt_pipeline* p) {
   Q.ry = to_dev(p, r.y);
   Q.rring = r.ring;
   Q.xin = r.xin;
+  Q.ytag = r.ytag;
+  Q.ldy = r.ldy;
   Q.rout = to_dev(p, r.out);
   Q.rdone = to_dev(p, r.done);
   if (p->d_trace) CUDA_TRY(cudaMemsetAsync(p->d_trace, 0, size_t(p->trace_cap) * sizeof(u64), p->stream));
@@ -1364,6 +1370,16 @@ int resident_step(pt_pipeline* p, const float* x, const float* y, float* out, fl
   std::atomic_thread_fence(std::memory_order_seq_cst);
   p->t_next = t + 1;
   const pt::PResDone d = *const_cast<const pt::PResDone*>(r.done);
+  static const bool dbg = getenv("PT_RESIDENT_DEBUG") != nullptr;  // diagnostics: per-step timing
+  if (dbg) {
+    static double dev_sum = 0, host_sum = 0;
+    static long cnt = 0;
+    dev_sum += double(d.done_ns - d.req_ns) * 1e-3;
+    host_sum += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t_begin).count();
+    if (++cnt % 100 == 0)
+      fprintf(stderr, "resident: %ld steps, device request->record %.1f us, host post->done %.1f us\n", cnt,
+              dev_sum / cnt, host_sum / cnt);
+  }
   if (out) memcpy(out, r.out + size_t(t & 1) * F, size_t(F) * 4);
   if (loss) *loss = d.loss;
   if (valid) *valid = d.valid;

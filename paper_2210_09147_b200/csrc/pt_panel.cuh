@@ -124,6 +124,8 @@ struct PParams {
   const float* ry;        // host-mapped target ring [rring][Fy]
   int rring;
   u64* xin;               // device: tagged stage-1 input [2][ldx]
+  u64* ytag;              // device: tagged targets [rring][ldy] (copied by CTA slices at the
+  int ldy;                //   tick they are posted; the loss reads them D-1 ticks later)
   float* rout;            // host-mapped outputs [2][F]
   struct PResDone* rdone; // host-mapped completion record
 };
@@ -139,6 +141,7 @@ struct PResDone {
   int valid;
   int status;
   int pad_;
+  unsigned long long req_ns, done_ns;  // diagnostics: globaltimer when CTA 0 saw the request / at the record
 };
 
 __device__ __forceinline__ int cmod4(long long t) { return int(t & 3); }  // two's complement: -1 -> 3
@@ -184,6 +187,7 @@ __device__ __forceinline__ bool pn_wait_request(const PParams& P, long long t, b
   long long r;
   if (poll_host) {
     while ((r = ld_acquire_sys_s64(P.hreq)) < t + 1 && r != PN_STOP) __nanosleep(64);
+    P.rdone->req_ns = globaltimer();
     if (ld_acquire_gpu_s64(P.relay) != r) st_release_gpu_s64(P.relay, r);
   } else {
     while ((r = ld_acquire_gpu_s64(P.relay)) < t + 1 && r != PN_STOP) __nanosleep(32);
@@ -685,6 +689,15 @@ __device__ __forceinline__ const float* pn_target(const PParams& P, long long si
   return P.yhist ? P.yhist + size_t(sid % P.yh) * Fy : nullptr;
 }
 
+// resident mode: the tagged device copy of sample sid's target, when it was posted during this
+// launch (earlier targets come from the target history ring, as in pt_run)
+__device__ __forceinline__ const u64* pn_ytag(const PParams& P, long long sid) {
+  return (P.resident && sid >= P.t0) ? P.ytag + size_t(sid % P.rring) * P.ldy : nullptr;
+}
+__device__ __forceinline__ float pn_y(const PParams& P, const float* y, const u64* yt, long long sid, int j) {
+  return yt ? pn_resolve(yt + j, ld_tv_gpu(yt + j), tag_of_tick(sid), false, P) : y[j];
+}
+
 // output row and loss partials of tick ti: per-run arrays, or two-tick rings (resident)
 __device__ __forceinline__ float* pn_outs(const PParams& P, int ti) {
   return P.resident ? P.rout + size_t((P.t0 + ti) & 1) * P.F : P.outs + size_t(ti) * P.F;  // host reads rout[t & 1]
@@ -709,39 +722,25 @@ __device__ __forceinline__ int pn_take(const PSmem& sm, int& cslot, uint32_t& cp
   return slot;
 }
 
-// Resident mode, last CTA of tick t: the epilogue kernel's loss (same summation order:
-// lane-strided partial sums, then the xor butterfly of warp_sum), validity, the non-finite
-// check, then the record's tick word last.
-__device__ __noinline__ void pn_resident_done(const PParams& P, long long t, int ti) {
+// Resident mode, last CTA of tick t (warp 0): the epilogue kernel's loss (same summation
+// order: lane-strided partial sums, then warp_sum), validity, the non-finite check, then the
+// record's tick word last.
+__device__ __noinline__ void pn_resident_done(const PParams& P, long long t, int ti, int lane) {
   __threadfence();
   const bool have = ld_volatile_s32(P.hflag) != 0;
   const bool v = t >= P.D - 1;
+  const float* lp = pn_lpart(P, ti);
   float s = 0.f;
-  if (v && have) {
-    const float* lp = pn_lpart(P, ti);
-    float acc[32];
-#pragma unroll
-    for (int l = 0; l < 32; ++l) {
-      float a = 0.f;
-      for (int c = l; c < P.G; c += 32) a += ldcg(lp + c);
-      acc[l] = a;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      float nx[32];
-#pragma unroll
-      for (int l = 0; l < 32; ++l) nx[l] = acc[l] + acc[l ^ o];
-#pragma unroll
-      for (int l = 0; l < 32; ++l) acc[l] = nx[l];
-    }
-    s = acc[0] * (P.loss == 1 ? 1.f : 1.f / float(P.F));
-  }
+  for (int c = lane; c < P.G; c += 32) s += ldcg(lp + c);
+  s = warp_sum(s) * (P.loss == 1 ? 1.f : 1.f / float(P.F));
+  if (lane != 0) return;
   PResDone* d = P.rdone;
   d->loss = (v && have) ? s : __int_as_float(0x7fc00000);
   d->valid = v ? 1 : 0;
   d->bad_loss = (v && have && !isfinite(s)) ? t : -1;
   d->bad_target = *reinterpret_cast<volatile long long*>(P.bad_target);
   d->status = ld_volatile_s32(P.status);
+  d->done_ns = globaltimer();
   __threadfence_system();
   *reinterpret_cast<volatile long long*>(&d->tick) = t + 1;
 }
@@ -869,6 +868,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constan
         u64* xd = P.xin + size_t(t & 1) * P.ldx;
         for (int j = bk0[4] + tid; j < bk0[5]; j += NCT) st_tv_gpu(xd + j, pack_tv(ld_volatile_f32(xr + j), tag_t));
       }
+      {
+        // this CTA's slice of gamma_t: mapped host memory -> the tagged target ring (padding
+        // words up to ldy are tagged zeros, so the loss gather can poll whole rows)
+        const Rows Y = rows_of(P.ldy, c, G);
+        const int Fy = P.loss == 1 ? 1 : P.F;
+        const float* yr = P.ry + size_t(t % P.rring) * Fy;
+        u64* yd = P.ytag + size_t(t % P.rring) * P.ldy;
+        for (int j = Y.r0 + tid; j < Y.r1; j += NCT) st_tv_gpu(yd + j, pack_tv(j < Fy ? ld_volatile_f32(yr + j) : 0.f, tag_t));
+      }
     }
     // tick barrier: every CTA finished tick t-1. It orders this tick's weight stores after
     // every read of their buffer (learning) and keeps the per-tick rings (cache slots mod 4,
@@ -991,6 +999,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constan
         const bool net_last = last && h == P.D;
         const long long sid = t - (P.D - 1);
         const float* y = net_last ? pn_target(P, sid, P.loss == 1 ? 1 : P.F) : nullptr;
+        const u64* yt = net_last ? pn_ytag(P, sid) : nullptr;
         float lsum = 0.f;
         int k = 0;
         for (int rb = RB.r0; rb < RB.r1; ++rb) {
@@ -1053,7 +1062,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constan
             if (net_last && row < P.F) {
               pn_outs(P, ti)[row] = a;
               if (P.loss == 0 && y) {
-                const float d = a - y[row];
+                const float d = a - pn_y(P, y, yt, sid, row);
                 lsum = fmaf(d, d, lsum);
               }
             }
@@ -1083,8 +1092,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constan
           for (int f = tid; f < P.F; f += NCT) se += expf(sm.va[f] - mx);
           se = pn_cta_red(se, false, sm);
           if (tid == 0) {
-            const int tgt = int(y[0]);
-            if (!(y[0] >= 0.f && y[0] < float(P.F) && float(tgt) == y[0])) {
+            const float y0 = pn_y(P, y, yt, sid, 0);
+            const int tgt = int(y0);
+            if (!(y0 >= 0.f && y0 < float(P.F) && float(tgt) == y0)) {
               atomicMin(P.bad_target, sid);
               pn_lpart(P, ti)[0] = 0.f;
             } else {
@@ -1128,6 +1138,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constan
         }
         const long long sid = t - (P.D - 1);
         const float* y = loss_src ? pn_target(P, sid, P.loss == 1 ? 1 : P.F) : nullptr;
+        const u64* yt = loss_src ? pn_ytag(P, sid) : nullptr;
+        // resident MSE: the targets join the gather as a second tagged vector
+        if (loss_src && yt && P.loss == 0) vg[1] = PV{yt, tag_of_tick(sid), 0};
         const float g_scale = 2.f / float(P.F);  // d mse / d a (M = 1)
         const float nlr = -P.lr;
         pn_gather<2>(vg, nout, P, [&](int j, const float (&x)[2][2]) {
@@ -1137,7 +1150,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constan
             if (loss_src) {
               const float a = x[0][e];
               if (P.loss == 1) d = a;  // raw output: softmax below
-              else d = (y && j + e < P.F) ? g_scale * (a - y[j + e]) * dact_fn(L.act, a) : 0.f;
+              else d = (y && j + e < P.F) ? g_scale * (a - (yt ? x[1][e] : y[j + e])) * dact_fn(L.act, a) : 0.f;
             } else if (stage_last) {
               d = x[0][e] * dact_fn(L.act, x[1][e]);
             } else {
@@ -1162,8 +1175,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constan
           int tgt = -1;
           bool ok = false;
           if (y) {
-            tgt = int(y[0]);
-            ok = y[0] >= 0.f && y[0] < float(P.F) && float(tgt) == y[0];
+            const float y0 = pn_y(P, y, yt, sid, 0);
+            tgt = int(y0);
+            ok = y0 >= 0.f && y0 < float(P.F) && float(tgt) == y0;
           }
           if (c == 0 && tid == 0 && y) {
             if (!ok) atomicMin(P.bad_target, sid);
@@ -1262,17 +1276,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constan
     // fenced for the producers' TMA loads, are published with it)
     if (P.learn) fence_proxy_async_global();
     cons_sync(NCT);
-    if (tid == 0) {
-      if (P.resident) {
+    if (P.resident) {
+      if (warp == 0) {
         // outputs went to host memory: make them visible system-wide before arriving; the
-        // last CTA to arrive completes the step for the host
-        __threadfence_system();
-        const u64 old = atomicAdd(reinterpret_cast<unsigned long long*>(P.tick_end), 1ull);
-        if (old + 1 == u64(G) * u64(t + 1)) pn_resident_done(P, t, ti);
-      } else {
-        __threadfence();
-        red_release_gpu(P.tick_end, 1);
+        // last CTA to arrive completes the step for the host (its warp 0 sums the loss)
+        bool last = false;
+        if (lane == 0) {
+          __threadfence_system();
+          const u64 old = atomicAdd(reinterpret_cast<unsigned long long*>(P.tick_end), 1ull);
+          last = old + 1 == u64(G) * u64(t + 1);
+        }
+        if (__shfl_sync(0xffffffffu, last, 0)) pn_resident_done(P, t, ti, lane);
       }
+    } else if (tid == 0) {
+      __threadfence();
+      red_release_gpu(P.tick_end, 1);
     }
     PN_TR(20);
   }

@@ -249,6 +249,8 @@ class Pipeline:
 
     def step(self, x_t, target_t=None) -> PipelineOutput:
         """pipeline_step: one synchronous tick."""
+        if type(x_t) is np.ndarray and (target_t is None or type(target_t) is np.ndarray):
+            return self._step_host(x_t, target_t)
         M, F = self.M, self.F
         dev = _is_cuda(x_t) or _is_cuda(target_t)
         x = None if x_t is None else _f32(x_t)
@@ -284,6 +286,37 @@ class Pipeline:
         lval = float(loss[0]) if (has_last and v and y is not None) else None
         o = out[0] if self._squeeze else out
         return PipelineOutput(step=t, output=o, loss=lval, valid=v, source_sample_id=t - (self.D - 1))
+
+    def _step_host(self, x_t, target_t):
+        """The per-sample host path with as little Python as possible: the library serves
+        consecutive steps from one resident launch, so the call overhead is the step's cost."""
+        M, F = self.M, self.F
+        x = x_t if (x_t.dtype == np.float32 and x_t.flags.c_contiguous) else _f32(x_t)
+        if x.size != M * self.dims[0]:
+            raise ValueError(f"x_t has shape {tuple(x.shape)}, expected [{M}, {self.dims[0]}]")
+        y = None
+        if target_t is not None:
+            y = target_t if (target_t.dtype == np.float32 and target_t.flags.c_contiguous) else _f32(target_t)
+            if y.size != M * self.Fy:
+                raise ValueError(f"target_t has shape {tuple(y.shape)}, expected [{M}, {self.Fy}]")
+            if self.Fy == 1:
+                self._check_targets(y, f"step {self._t}")
+        out = np.empty((M, F), np.float32)
+        sc = getattr(self, "_scalars", None)
+        if sc is None:
+            sc = self._scalars = (np.empty(1, np.float32), np.empty(1, np.int32))
+        loss, valid = sc
+        rc = self._lib.pt_step(self._h, x.ctypes.data, None if y is None else y.ctypes.data, out.ctypes.data,
+                               loss.ctypes.data, valid.ctypes.data, _lib.PT_HOST)
+        t = self._t
+        self._t += 1
+        if rc:
+            _lib.check(rc, f"pipeline_step at step {t}")
+        has_last = self.local_first + self.local_count == self.D
+        v = bool(valid[0]) if has_last else t >= self.D - 1
+        lval = float(loss[0]) if (has_last and v and y is not None) else None
+        return PipelineOutput(step=t, output=out[0] if self._squeeze else out, loss=lval, valid=v,
+                              source_sample_id=t - (self.D - 1))
 
     def run(self, xs, ys=None, n=None):
         """n ticks with no per-tick host round trip (pt_run). xs [n, M, d0], ys [n, M, F]
