@@ -8,7 +8,13 @@ KEYS = ["dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__dram_throughput.a
         "launch__grid_size", "launch__registers_per_thread", "launch__shared_mem_per_block_dynamic",
         "lts__t_sector_hit_rate.pct", "sm__inst_executed_pipe_tensor_subpipe_hmma.avg.pct_of_peak_sustained_active",
         "sm__throughput.avg.pct_of_peak_sustained_elapsed", "sm__warps_active.avg.pct_of_peak_sustained_active",
-        "smsp__inst_executed.sum", "sm__pipe_tensor_op_hmma_cycles_active.avg.pct_of_peak_sustained_active"]
+        "smsp__inst_executed.sum", "sm__pipe_tensor_op_hmma_cycles_active.avg.pct_of_peak_sustained_active",
+        # tcgen05 (UTCHMMA) activity: the hmma subpipe metrics above only count legacy mma.sync
+        "sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__ops_path_tensor_op_utchmma_src_tf32_dst_fp32_sparsity_off.sum.pct_of_peak_sustained_elapsed",
+        "smsp__sass_inst_executed_op_utcmma.sum", "smsp__sass_inst_executed_op_tmem_ldt.sum",
+        "smsp__sass_inst_executed_op_tmem_stt.sum", "lts__throughput.avg.pct_of_peak_sustained_elapsed"]
 UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
 
