@@ -655,11 +655,15 @@ int upload_panel_desc(pt_pipeline* p) {
     memset(&d, 0, sizeof(d));
     for (int j = 0; j < 2; ++j) {
       d.W[j] = h.Wt[j] ? h.Wt[j] : h.Wt[0];
-      d.tm[j] = p->d_pmaps ? p->d_pmaps + 2 * i + j : nullptr;
+      d.tm[j] = p->d_pmaps ? p->d_pmaps + 4 * i + j : nullptr;
       d.gin[j] = h.gin[j];
     }
     d.b = h.b;
     d.dpl = h.dpl;
+    d.mW = h.mW;
+    d.vW = h.vW;
+    d.mb = h.mb;
+    d.vb = h.vb;
     d.bw = h.bw;
     d.n_in = h.n_in;
     d.n_out = h.n_out;
@@ -759,7 +763,7 @@ int setup_panel(pt_pipeline* p) {
       // every layer but the network's first reads W in the backward and updates it there; the
       // first layer's update is deferred to the next forward, which needs its delta a tick later
       // (plain [2][R*16]). gin: the tagged delta of the previous layer this backward publishes.
-      Lh.bw = li_global != 0;
+      Lh.bw = li_global != 0 || p->opt == PT_OPT_ADAM;
       if (!Lh.bw)
         PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&Lh.dpl), size_t(2) * Lh.R * pt::PN_TS * sizeof(float)));
       else
@@ -768,11 +772,14 @@ int setup_panel(pt_pipeline* p) {
     }
   }
   if (p->learn) {
-    std::vector<CUtensorMap> maps(2 * p->layers.size());
-    for (size_t i = 0; i < p->layers.size(); ++i)
+    std::vector<CUtensorMap> maps(4 * p->layers.size());  // per layer: W[0], W[1] (2 spare)
+    for (size_t i = 0; i < p->layers.size(); ++i) {
+      const LayerHost& Lh = p->layers[i];
+      const float* src[2] = {Lh.Wt[0], Lh.Wt[1]};
       for (int j = 0; j < 2; ++j)
-        if (panel_tmap(&maps[2 * i + j], p->layers[i].Wt[j], p->layers[i].R, p->layers[i].C))
+        if (src[j] && panel_tmap(&maps[4 * i + j], src[j], Lh.R, Lh.C))
           return fail(PT_ECUDA, "cuTensorMapEncodeTiled failed for layer " + std::to_string(p->layer_base + i));
+    }
     PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&p->d_pmaps), maps.size() * sizeof(CUtensorMap)));
     CUDA_TRY(cudaMemcpy(p->d_pmaps, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
   }
@@ -790,7 +797,7 @@ int setup_panel(pt_pipeline* p) {
   const int slot_bytes = pt::PN_SLOT_FLOATS * 4;
   int nslot = std::min(pt::PN_MAXSLOT, (pt::SMEM_MAX - tail) / slot_bytes);
   if (const char* e = getenv("PT_NSLOT")) nslot = std::min(nslot, std::max(2, atoi(e)));
-  if (nslot < 2)
+  if (nslot < 2 || (p->opt == PT_OPT_ADAM && nslot < 3))  // an Adam backward chunk holds 3 slots
     return fail(PT_EINVAL, "shared memory too small for this layer shape (rows per CTA); use a larger grid");
   p->pn_nslot = nslot;
   int off = nslot * slot_bytes;
@@ -814,6 +821,7 @@ int setup_panel(pt_pipeline* p) {
   if (const char* e = getenv("PT_PF_CHUNKS")) p->pn_pf = std::max(0, atoi(e));
   if (p->pn_smem > pt::SMEM_MAX) return fail(PT_EINVAL, "panel shared-memory plan exceeds 227 KB");
   CUDA_TRY(cudaFuncSetAttribute(pt::panel_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, pt::SMEM_MAX));
+  CUDA_TRY(cudaFuncSetAttribute(pt::panel_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, pt::SMEM_MAX));
   return PT_OK;
 }
 
@@ -875,7 +883,8 @@ int create_impl(const pt_config* c, pt_pipeline* p) {
     // first launch of a kernel may wait for the kernels running on the device; a persistent
     // stage kernel waiting for a neighbour (another handle, part or process) that is itself
     // blocked in such a load would only end at the watchdog.
-    const void* others[] = {(const void*)pt::panel_kernel<0>, (const void*)pt::tile_kernel<0>,
+    const void* others[] = {(const void*)pt::panel_kernel<0>, (const void*)pt::panel_kernel<1>,
+                            (const void*)pt::tile_kernel<0>,
                             (const void*)pt::tile_kernel<1>,
                             (const void*)pt::epilogue_kernel, (const void*)pt::pn_to_tiles,
                             (const void*)pt::pn_from_tiles};
@@ -903,7 +912,7 @@ int create_impl(const pt_config* c, pt_pipeline* p) {
   {
     // batch-1 panel path (pt_panel.cuh): SGD, any widths; stages in turn on every CTA.
     // PT_PANEL=0 keeps the row-owned tick kernel.
-    bool ok = !p->tile && p->M == 1 && p->opt == PT_OPT_SGD;
+    bool ok = !p->tile && p->M == 1;  // SGD or Adam
     if (const char* e = getenv("PT_PANEL")) ok = ok && atoi(e) != 0;
     if (ok) {
       p->panel = true;
@@ -933,8 +942,10 @@ int create_impl(const pt_config* c, pt_pipeline* p) {
     }
     PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&Lh.b), size_t(Lh.n_out) * 4));
     if (p->opt == PT_OPT_ADAM && p->learn) {
-      PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&Lh.mW), size_t(Lh.n_out) * Lh.ld_in * 4));
-      PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&Lh.vW), size_t(Lh.n_out) * Lh.ld_in * 4));
+      // moments in the weights' layout: row-major [n_out][ld_in], or the panel path's tiles
+      const size_t nm = p->panel ? size_t(Lh.R) * Lh.C * pt::PN_TILE : size_t(Lh.n_out) * Lh.ld_in;
+      PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&Lh.mW), nm * 4));
+      PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&Lh.vW), nm * 4));
       PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&Lh.mb), size_t(Lh.n_out) * 4));
       PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&Lh.vb), size_t(Lh.n_out) * 4));
     }
@@ -1146,6 +1157,14 @@ void panel_common(pt_pipeline* p, pt::PParams& Q) {
   Q.F = p->F();
   Q.loss = p->loss;
   Q.lr = p->lr;
+  Q.b1 = 0.9f;  // Adam (oracle/netcore.py Adam), as the tick kernel
+  Q.b2 = 0.999f;
+  Q.b1d = 0.9;
+  Q.b2d = 0.999;
+  Q.omb1 = float(1.0 - 0.9);
+  Q.omb2 = float(1.0 - 0.999);
+  Q.eps = 1e-8f;
+  Q.adam = p->opt == PT_OPT_ADAM && p->learn ? 1 : 0;
   Q.ldx = p->stage_ld0(0);
   Q.yhist = p->yhist;
   Q.yh = p->yh;
@@ -1291,7 +1310,8 @@ int resident_start(pt_pipeline* p) {
   Q.rdone = to_dev(p, r.done);
   if (p->d_trace) CUDA_TRY(cudaMemsetAsync(p->d_trace, 0, size_t(p->trace_cap) * sizeof(u64), p->stream));
   void* qargs[] = {&Q};
-  CUDA_TRY(cudaLaunchCooperativeKernel((const void*)pt::panel_kernel<0>, dim3(p->G), dim3(pt::NTHREADS), qargs,
+  CUDA_TRY(cudaLaunchCooperativeKernel(p->opt == PT_OPT_ADAM ? (const void*)pt::panel_kernel<1> : (const void*)pt::panel_kernel<0>,
+                                       dim3(p->G), dim3(pt::NTHREADS), qargs,
                                        size_t(p->pn_smem), p->stream));
   r.on = true;
   r.t_start = p->t_next;
@@ -1565,7 +1585,8 @@ int run_impl(pt_pipeline* p, const float* xs, const float* ys, int64_t n, float*
     Q.jitter_mask = P.jitter_mask;
     void* qargs[] = {&Q};
     CUDA_TRY(cudaEventRecord(p->ev0, p->stream));
-    CUDA_TRY(cudaLaunchCooperativeKernel((const void*)pt::panel_kernel<0>, dim3(p->G), dim3(pt::NTHREADS), qargs,
+    CUDA_TRY(cudaLaunchCooperativeKernel(p->opt == PT_OPT_ADAM ? (const void*)pt::panel_kernel<1> : (const void*)pt::panel_kernel<0>,
+                                       dim3(p->G), dim3(pt::NTHREADS), qargs,
                                          size_t(p->pn_smem), p->stream));
     CUDA_TRY(cudaEventRecord(p->ev1, p->stream));
   } else if (p->tile) {

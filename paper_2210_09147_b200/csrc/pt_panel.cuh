@@ -60,6 +60,10 @@ struct PLayer {
   float* b;                  // bias [n_out] (the owner CTA keeps its rows in smem during a launch)
   u64* gin[2];               // tagged delta of the previous layer = act' * g_in, [C*16] per tick parity
   float* dpl;                // plain copy of this layer's delta, [2][R*16] per tick parity (read at t+1)
+  float *mW, *vW;            // Adam moments, 16 x 16 tiles in column-panel-major order (tile (rb, cb) at
+                             // (cb * R + rb) * 256): only the backward touches them, one column
+                             // panel per CTA, so a chunk is 32 KB contiguous (one bulk copy)
+  float *mb, *vb;            // Adam moments of the bias [n_out]
   int n_in, n_out, R, C, act;
   int bw;                    // learning, and the backward reads W: it applies the update and stores
                              // W^(t+1) (buffer (t+1)&1); else the forward applies it (deferred)
@@ -88,6 +92,9 @@ struct PParams {
   const PLayer* layers;
   int n_stages, n_layers, D, learn, act_delay, G, F, loss;
   float lr;
+  float b1, b2, eps, omb1, omb2;  // Adam, as pt::Params
+  double b1d, b2d;
+  int adam;  // Adam: an updating backward chunk occupies three ring slots (W, m, v)
   const float* xs;  // padded [n][ldx] (stage 1 local)
   int ldx;
   const float* ys;  // [n][Fy] targets of this run
@@ -407,7 +414,7 @@ struct PCursor {
       R = Rows{b[0], b[1]};
       len = L->C;
     } else {
-      R = (S.h == 1 && i == 0) ? Rows{0, 0} : Rows{b[2], b[3]};
+      R = (S.h == 1 && i == 0 && !L->bw) ? Rows{0, 0} : Rows{b[2], b[3]};
       len = L->R;
     }
     b0 = R.r0;
@@ -477,6 +484,11 @@ __device__ void pn_producer(const PParams& P, const PLayer* layers, const PStage
         prefetch_l2(pf.L->W[pn_fbuf(P, *pf.L, t)] + pf.foff(), uint32_t(pf.ntiles()) * PN_TILE * 4u);
       } else {
         pn_tma_prefetch_3d(pf.L->tm[int(t & 1)], 0, pf.blk, pf.off);
+        if (P.adam && pn_upd(P, stages[pf.s].h, t)) {
+          const size_t o = (size_t(pf.blk) * pf.L->R + pf.off) * PN_TILE;
+          prefetch_l2(pf.L->mW + o, uint32_t(pf.ntiles()) * PN_TILE * 4u);
+          prefetch_l2(pf.L->vW + o, uint32_t(pf.ntiles()) * PN_TILE * 4u);
+        }
       }
       pf.advance(P, stages, layers);
       ++pf_idx;
@@ -519,30 +531,44 @@ __device__ void pn_producer(const PParams& P, const PLayer* layers, const PStage
         raw_ti = ti;
       }
     }
-    const int slot = int(chunk % uint32_t(nslot));
-    const uint32_t use = chunk / uint32_t(nslot);
-    if (use > 0) {
-      const uint64_t t0 = globaltimer();
-      while (!dead && !mbar_try_wait(&empty[slot], (use - 1) & 1u)) {
-        top_up();
-        if (P.psleep) __nanosleep(P.psleep);  // leave issue slots to the consumer warps of this SMSP
-        if (pn_watchdog(P, t0)) dead = true;
+    // an updating Adam backward chunk loads W, m and v into three consecutive ring slots
+    const int nparts = (P.adam && !cur.fwd() && pn_upd(P, stages[cur.s].h, t)) ? 3 : 1;
+    for (int part = 0; part < nparts && !dead; ++part) {
+      const int slot = int(chunk % uint32_t(nslot));
+      const uint32_t use = chunk / uint32_t(nslot);
+      if (use > 0) {
+        const uint64_t t0 = globaltimer();
+        while (!dead && !mbar_try_wait(&empty[slot], (use - 1) & 1u)) {
+          top_up();
+          if (P.psleep) __nanosleep(P.psleep);  // leave issue slots to the consumer warps of this SMSP
+          if (pn_watchdog(P, t0)) dead = true;
+        }
       }
+      if (dead) break;
+      float* sdst = ring + size_t(slot) * PN_SLOT_FLOATS;
+      if (cur.fwd()) {
+        pn_trace(P, tr, P.trace_cap - P.trace_cap / 4, 40);
+        pn_jitter(P, 40);
+        const uint32_t bytes = uint32_t(cur.ntiles()) * PN_TILE * 4u;
+        mbar_arrive_expect_tx(&full[slot], bytes);
+        bulk_g2s(sdst, cur.L->W[pn_fbuf(P, *cur.L, t)] + cur.foff(), bytes, &full[slot], pol);
+      } else {
+        pn_trace(P, tr, P.trace_cap - P.trace_cap / 4, 41);
+        pn_jitter(P, 41);
+        if (part == 0) {
+          mbar_arrive_expect_tx(&full[slot], uint32_t(PN_SLOT_FLOATS) * 4u);
+          pn_tma_load_3d(sdst, cur.L->tm[int(t & 1)], 0, cur.blk, cur.off, &full[slot], pol);
+        } else {
+          // Adam moments: the chunk is contiguous in their column-panel-major layout
+          const uint32_t bytes = uint32_t(cur.ntiles()) * PN_TILE * 4u;
+          const float* src = (part == 1 ? cur.L->mW : cur.L->vW) + (size_t(cur.blk) * cur.L->R + cur.off) * PN_TILE;
+          mbar_arrive_expect_tx(&full[slot], bytes);
+          bulk_g2s(sdst, src, bytes, &full[slot], pol);
+        }
+      }
+      if (part + 1 < nparts) ++chunk;
     }
     if (dead) break;
-    float* sdst = ring + size_t(slot) * PN_SLOT_FLOATS;
-    if (cur.fwd()) {
-      pn_trace(P, tr, P.trace_cap - P.trace_cap / 4, 40);
-      pn_jitter(P, 40);
-      const uint32_t bytes = uint32_t(cur.ntiles()) * PN_TILE * 4u;
-      mbar_arrive_expect_tx(&full[slot], bytes);
-      bulk_g2s(sdst, cur.L->W[pn_fbuf(P, *cur.L, t)] + cur.foff(), bytes, &full[slot], pol);
-    } else {
-      pn_trace(P, tr, P.trace_cap - P.trace_cap / 4, 41);
-      pn_jitter(P, 41);
-      mbar_arrive_expect_tx(&full[slot], uint32_t(PN_SLOT_FLOATS) * 4u);
-      pn_tma_load_3d(sdst, cur.L->tm[int(t & 1)], 0, cur.blk, cur.off, &full[slot], pol);
-    }
     ++chunk;
     cur.advance(P, stages, layers);
     top_up();
@@ -635,6 +661,61 @@ __device__ __forceinline__ void pn_fdot(const float* wb, const float* va, int nt
 // Backward chunk: acc += W^(t)[rows][own 4 columns] * delta[rows] (this thread: float4 f4 of
 // row tr of tiles tg, tg+4, ...), and W^(t+1) = W^(t) - lr delta[row] a_hat[col] stored to the
 // next buffer (UPD; the plain copy otherwise, during the warm-up)
+__device__ __forceinline__ float pn_adam1(float w, float g, float& m, float& v, const PParams& P, float c1, float c2) {
+  m = fmaf(P.b1, m, P.omb1 * g);
+  v = fmaf(P.b2, v, P.omb2 * g * g);
+  return w - P.lr * adam_quot(m * c1, v * c2, P.eps);
+}
+__device__ __forceinline__ void pn_adam4(float4& w, float d, float4 ah, float4& m, float4& v, const PParams& P,
+                                         float c1, float c2) {
+  w.x = pn_adam1(w.x, d * ah.x, m.x, v.x, P, c1, c2);
+  w.y = pn_adam1(w.y, d * ah.y, m.y, v.y, P, c1, c2);
+  w.z = pn_adam1(w.z, d * ah.z, m.z, v.z, P, c1, c2);
+  w.w = pn_adam1(w.w, d * ah.w, m.w, v.w, P, c1, c2);
+}
+
+// Backward chunk with the Adam step: g_in from the pre-update W as in pn_bchunk,
+// then per weight g = delta_r * a_hat_c and the moments of the same tiled position, read and
+// written in place (their loads are issued before the shared-memory tile is read). GIN: this
+// layer publishes g_in (else: the network's first layer, update only).
+template <bool FULL, bool GIN>
+__device__ __forceinline__ void pn_bchunk_adam(const float* wb, const float* dl, float4 ah4, float* gdst, const float* ms,
+                                               const float* vs, float* mdst, float* vdst, int C, int nt, int tg,
+                                               float4& acc, const PParams& P, float c1, float c2) {
+#pragma unroll
+  for (int hh = 0; hh < 2; ++hh) {
+    float4 w[4];
+    float d[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int tt = (hh * 4 + q) * 4 + tg;
+      const bool ok = FULL || tt < nt;
+      w[q] = ok ? lds4(wb + tt * PN_TILE) : make_float4(0.f, 0.f, 0.f, 0.f);
+      d[q] = ok ? dl[tt * PN_TS] : 0.f;
+    }
+    if (GIN) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        acc.x = fmaf(w[q].x, d[q], acc.x);
+        acc.y = fmaf(w[q].y, d[q], acc.y);
+        acc.z = fmaf(w[q].z, d[q], acc.z);
+        acc.w = fmaf(w[q].w, d[q], acc.w);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int tt = (hh * 4 + q) * 4 + tg;
+      if (FULL || tt < nt) {
+        float4 m = lds4(ms + tt * PN_TILE), v = lds4(vs + tt * PN_TILE);
+        pn_adam4(w[q], d[q], ah4, m, v, P, c1, c2);
+        __stcs(reinterpret_cast<float4*>(gdst + size_t(tt) * C * PN_TILE), w[q]);
+        __stcg(reinterpret_cast<float4*>(mdst + size_t(tt) * PN_TILE), m);  // consecutive tiles
+        __stcg(reinterpret_cast<float4*>(vdst + size_t(tt) * PN_TILE), v);
+      }
+    }
+  }
+}
+
 template <bool UPD, bool FULL>
 __device__ __forceinline__ void pn_bchunk(const float* wb, const float* dl, float nlr, float4 ah4, float* gdst,
                                           int C, int nt, int tg, float4& acc) {
@@ -745,7 +826,8 @@ __device__ __noinline__ void pn_resident_done(const PParams& P, long long t, int
   *reinterpret_cast<volatile long long*>(&d->tick) = t + 1;
 }
 
-template <int DUMMY>
+// OPT: 0 SGD, 1 Adam (every layer then updates in its backward, the network's first included)
+template <int OPT>
 __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constant__ PParams P) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   PSmem sm;
@@ -823,6 +905,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constan
         for (int b = 0; b < 2; ++b) {
           tma_fence_desc_acquire(s_layers[l].tm[b]);
           tma_prefetch_desc(s_layers[l].tm[b]);
+
         }
       pn_producer(P, s_layers, s_stages, sm.ring, sm.full, sm.empty, sm.flags, nF, sm.blk);
     }
@@ -1108,6 +1191,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constan
       const bool upd_now = pn_upd(P, h, t);
       const long long Ct = pn_ct(P, h, t);
       u64* Cc = S.cache[cmod4(Ct)];
+      // Adam bias corrections of this stage's k-th update (k counts from the warm-up gate;
+      // in double, as pt::tick_kernel)
+      float c1 = 1.f, c2 = 1.f;
+      if (OPT == 1 && upd_now) {
+        const double k = double(t - (2LL * P.D - h - 1) + 1);
+        c1 = float(1.0 / (1.0 - pow(P.b1d, k)));
+        c2 = float(1.0 / (1.0 - pow(P.b2d, k)));
+      }
       for (int i = S.k - 1; i >= 0; --i) {
         const PLayer& L = s_layers[S.first + i];
         const int nout = L.R * PN_TS;
@@ -1115,13 +1206,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constan
         const Rows RB{bk[0], bk[1]};
         const Rows CB{bk[2], bk[3]};
         const int ncol = (CB.r1 - CB.r0) * PN_TS;
-        const bool need_gin = !(h == 1 && i == 0);  // else: no weight read (and no update here: L.bw == 0)
+        const bool need_gin = !(h == 1 && i == 0);  // the network's first layer publishes no g_in
+        // weight chunks: every layer with a g_in, and the first layer when it updates in the
+        // backward (Adam); SGD defers the first layer's update to the next forward (L.bw == 0)
+        const bool do_chunks = need_gin || L.bw;
         const bool stage_last = i == S.k - 1;
         const bool loss_src = stage_last && h == P.D;
         PN_TR(11);
         // a_hat_t of own columns (this layer's input at the cache tick): loads issued here,
         // resolved after the gather
-        const u64* ahp = (need_gin && upd_now) ? Cc + L.cache_in + CB.r0 * PN_TS : nullptr;
+        const u64* ahp = (do_chunks && upd_now) ? Cc + L.cache_in + CB.r0 * PN_TS : nullptr;
         const u64 ah = (ahp && tid < ncol) ? ld_tv_gpu(ahp + tid) : 0ull;
         // delta_l(t): the next layer's published vector, or (stage's last layer) the loss
         // gradient / the downstream stage's g_in times act'; delta_l(t-1) for the rebuild
@@ -1196,11 +1290,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constan
           if (stage_last && !L.bw) L.dpl[size_t(t & 1) * nout + j] = d;  // forward-applied update at t+1
           if (upd_now && j < L.n_out) {
             float* bp = sm.bias + sm.boff[S.first + i] + (j - RB.r0 * PN_TS);
-            *bp = fmaf(nlr, d, *bp);
+            if (OPT == 1) {
+              float mm = __ldcg(L.mb + j), vv = __ldcg(L.vb + j);
+              *bp = pn_adam1(*bp, d, mm, vv, P, c1, c2);
+              __stcg(L.mb + j, mm);
+              __stcg(L.vb + j, vv);
+            } else {
+              *bp = fmaf(nlr, d, *bp);
+            }
           }
         }
         PN_TR(13);
-        if (need_gin) {
+        if (do_chunks) {
           const bool to_peer = (i == 0);  // first layer of stage h > 1: g_in goes upstream (no act')
           const PLayer* Lp = to_peer ? nullptr : &s_layers[S.first + i - 1];
           for (int cb = CB.r0; cb < CB.r1; ++cb) {
@@ -1214,6 +1315,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constan
             const float4 ah4 = upd_now ? lds4(sm.sah + (cb - CB.r0) * PN_TS + f4 * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
             float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
             float* Wn = L.W[int((t + 1) & 1)] + size_t(cb) * PN_TILE + toff;  // W^(t+1), this column panel
+            // Adam moments of this column panel (column-panel-major: consecutive tiles)
+            float* Mn = OPT == 1 ? L.mW + size_t(cb) * L.R * PN_TILE + toff : nullptr;
+            float* Vn = OPT == 1 ? L.vW + size_t(cb) * L.R * PN_TILE + toff : nullptr;
             for (int j0 = 0; j0 < L.R; j0 += PN_CT) {
               const int nt = min(PN_CT, L.R - j0);
               const int slot = pn_take(sm, cslot, cphase, P);
@@ -1221,7 +1325,29 @@ __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constan
               const float* wb = sm.ring + size_t(slot) * PN_SLOT_FLOATS + toff;
               const float* dl = sm.va + j0 * PN_TS + tr;
               float* gd = Wn + size_t(j0) * L.C * PN_TILE;
-              if (upd_now) {
+              if (OPT == 1 && upd_now) {
+                // the chunk's moments arrived in the next two ring slots (pn_producer)
+                const int mslot = pn_take(sm, cslot, cphase, P);
+                const int vslot = pn_take(sm, cslot, cphase, P);
+                PN_TRC(50);
+                const float* ms = sm.ring + size_t(mslot) * PN_SLOT_FLOATS + toff;
+                const float* vs = sm.ring + size_t(vslot) * PN_SLOT_FLOATS + toff;
+                float* md = Mn + size_t(j0) * PN_TILE;
+                float* vd = Vn + size_t(j0) * PN_TILE;
+                if (need_gin) {
+                  if (nt == PN_CT) pn_bchunk_adam<true, true>(wb, dl, ah4, gd, ms, vs, md, vd, L.C, nt, tg, acc, P, c1, c2);
+                  else pn_bchunk_adam<false, true>(wb, dl, ah4, gd, ms, vs, md, vd, L.C, nt, tg, acc, P, c1, c2);
+                } else {
+                  if (nt == PN_CT) pn_bchunk_adam<true, false>(wb, dl, ah4, gd, ms, vs, md, vd, L.C, nt, tg, acc, P, c1, c2);
+                  else pn_bchunk_adam<false, false>(wb, dl, ah4, gd, ms, vs, md, vd, L.C, nt, tg, acc, P, c1, c2);
+                }
+                PN_TRC(51);
+                __syncwarp();
+                if (lane == 0) {
+                  mbar_arrive(&sm.empty[mslot]);
+                  mbar_arrive(&sm.empty[vslot]);
+                }
+              } else if (upd_now) {
                 if (nt == PN_CT) pn_bchunk<true, true>(wb, dl, nlr, ah4, gd, L.C, nt, tg, acc);
                 else pn_bchunk<true, false>(wb, dl, nlr, ah4, gd, L.C, nt, tg, acc);
               } else {
@@ -1231,6 +1357,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constan
               __syncwarp();
               if (lane == 0) mbar_arrive(&sm.empty[slot]);
             }
+            if (!need_gin) continue;  // the network's first layer (Adam): update only
             // column sums over tr (lane bits 2-4, warp bit 0) and tg (warp bits 1-2)
             float g[4] = {acc.x, acc.y, acc.z, acc.w};
 #pragma unroll
@@ -1268,7 +1395,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constan
             }
           }
         }
-        if (!need_gin || CB.r0 == CB.r1) cons_sync(NCT);  // no chunk loop: the delta store's reads of va are done
+        // no chunk loop (or none with a reduction): the delta store's reads of va are done
+        if (!need_gin || CB.r0 == CB.r1) cons_sync(NCT);
         PN_TR(14);
       }
     }

@@ -518,7 +518,7 @@ __device__ __forceinline__ void t_lo_pass_b(const float* tile, uint32_t lo_tmem)
 __device__ __forceinline__ float t_adam1(float w, float g, float& m, float& v, const TParams& P, float c1, float c2) {
   m = fmaf(P.b1, m, P.omb1 * g);
   v = fmaf(P.b2, v, P.omb2 * g * g);
-  return w - P.lr * (m * c1) / (sqrtf(v * c2) + P.eps);
+  return w - P.lr * adam_quot(m * c1, v * c2, P.eps);
 }
 
 template <bool ADAM>

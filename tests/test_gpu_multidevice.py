@@ -78,7 +78,7 @@ def test_virtual_devices_match_single_device(virtual_devices, widths, counts, de
     import torch
     grid = torch.cuda.get_device_properties(0).multi_processor_count // len(devices)
     kind = _compare(widths, counts, devices, T, M=M, opt=opt, grid=grid, lr=0.02 if opt == "sgd" else 1e-3)
-    assert kind == {1: {"sgd": "panel", "adam": "tick"}, 16: {"sgd": "tile"}}[M][opt]
+    assert kind == {1: "panel", 16: "tile"}[M]
 
 
 def test_virtual_devices_step_api(virtual_devices):

@@ -416,6 +416,20 @@ def test_adam(D):
     _case([24, 40, 32, 12], counts, 30, 1e-3, optimizer="adam")
 
 
+@pytest.mark.parametrize("kernel", ["panel", "tick"])
+def test_adam_batch1_kernels(kernel, monkeypatch):
+    """Adam at batch 1 on the panel kernel (every layer updates in its backward, the network's
+    first included) and on the row-owned tick kernel (PT_PANEL=0); D=3, softmax-CE too."""
+    if kernel == "tick":
+        monkeypatch.setenv("PT_PANEL", "0")
+    m = mdl.mlp([48, 96, 64, 80, 10], seed=2)
+    p = engine.Pipeline(m, [2, 2, 3], "adam", 1e-3, np.zeros(48, np.float32), np.zeros(10, np.float32))
+    assert p.kernel_path == kernel
+    p.close()
+    _case([48, 96, 64, 80, 10], [2, 2, 3], 30, 1e-3, optimizer="adam")
+    _case([48, 96, 64, 80, 10], [2, 2, 3], 30, 1e-3, optimizer="adam", loss="softmax_ce", act_delay=0)
+
+
 @pytest.mark.parametrize("D", [1, 2])
 def test_softmax_ce(D):
     counts = {1: [5], 2: [2, 3]}[D]

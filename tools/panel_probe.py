@@ -21,7 +21,8 @@ def main():
     st = streams.SmoothStream(W, W, seed=1)
     xs, ys = st.block(0, T)
     xs, ys = xs.astype(np.float32), ys.astype(np.float32)
-    p = engine.Pipeline(m, [len(m.layers)], "sgd", 1e-3, xs[0, 0], ys[0, 0])
+    opt = sys.argv[4] if len(sys.argv) > 4 else "sgd"
+    p = engine.Pipeline(m, [len(m.layers)], opt, 1e-3 if opt == "sgd" else 1e-4, xs[0, 0], ys[0, 0])
     print("path", p.kernel_path)
     p.run(xs, ys)
     p.sync()
