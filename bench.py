@@ -214,7 +214,9 @@ def extra_configs(peak):
     import torch
     from paper_2210_09147_b200 import engine, model as mdl, streams
     c5 = [1024, 2048, 4096, 8192, 8192, 4096, 2048, 1024] * 3 + [1024]
-    cases = [("C3", "64-layer 4096-wide MLP inference wave, D=8 stages on 1 GPU", [4096] * 65, 8, False, 1, 8,
+    cases = [("C2_adam", "C2 (32-layer 2048-wide, batch 1, D=1) with Adam", [2048] * 33, 1, True, 1, 32,
+              "adam", "mse"),
+             ("C3", "64-layer 4096-wide MLP inference wave, D=8 stages on 1 GPU", [4096] * 65, 8, False, 1, 8,
               "sgd", "mse"),
              ("C4", "32-layer 4096-wide MLP, micro-batch 16, D=8 stages on 1 GPU", [4096] * 33, 8, True, 16, 8,
               "sgd", "mse"),

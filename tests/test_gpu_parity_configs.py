@@ -35,6 +35,11 @@ def test_c2_50_ticks(D):
     _case([2048] * 33, bench.plan_counts(32, D), 50, 1e-3)
 
 
+def test_c2_adam_d1():
+    """Config 2's shape with Adam on the panel kernel (a bench other_configs line), 12 ticks."""
+    _case([2048] * 33, [63], 12, 1e-4, optimizer="adam")
+
+
 def test_c3_inference_d8():
     """Config 3: 64 x 4096 inference-only forward wave, D = 8 (bench split), 16 ticks."""
     w = [4096] * 65
