@@ -1,4 +1,4 @@
-// pt_panel.cuh: the batch-1 panel kernel for sm_100a (SGD; MSE or softmax-CE).
+// pt_panel.cuh: the batch-1 panel kernel for sm_100a (SGD or Adam; MSE or softmax-CE).
 //
 // Same tick contract as pt::tick_kernel (reference SPEC.md:217-225,
 // 253-257), with a weight layout and work split that take the backward's
@@ -16,14 +16,14 @@
 // Both steps end in an all-gather of a tagged vector (every CTA needs the whole previous
 // vector); no step has a cross-CTA reduction.
 //
-// Deferred update. B_l(t) only READS W^(t) (4 B/weight). The rank-1 update
-// W^(t+1) = W^(t) - lr delta_t a_hat_t^T is applied by F_l(t+1) to each tile as soon as it
-// lands in shared memory, before F's input vector is there ("update-ahead"), and the
-// consumer threads store the result straight to the other buffer (8 B/weight): 12 B/weight
-// per tick, the algorithmic bytes of the fused tick kernel. F_l(t) reads buffer (t-1)&1 and
-// writes buffer t&1; B_l(t) reads buffer (t-1)&1 too and rebuilds W^(t) element by element
-// with the same fmaf F used, so both see bit-identical weights. The pending update of a
-// run's last tick is applied by the next run's F (or by pt_get_params).
+// Update placement. B_l(t) reads W^(t) (the pre-update weights g_in needs), applies the
+// rank-1 step W^(t+1) = W^(t) - lr delta_t a_hat_t^T in registers and stores W^(t+1) into the
+// other buffer; F_l(t+1) then reads it (4 + 8 B/weight per tick). The network's first layer has
+// no g_in and hence no backward weight read, so with SGD its update is deferred: F_0(t+1)
+// applies it to each chunk as it lands in shared memory, before the input vector is there
+// ("update-ahead"), and stores W^(t+1) (8 B/weight); the pending update of a run's last tick is
+// applied by the next run's forward, or by pt_get_params. With Adam every layer updates in its
+// backward, and the moments stream through the ring beside W (PLayer::mW).
 //
 // Backward vectors. The CTA that publishes g_in of layer l+1 for its columns multiplies by
 // act'(a_l) itself, so the published vector IS delta_l (tagged, tick parity). It is the
