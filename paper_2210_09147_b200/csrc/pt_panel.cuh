@@ -465,6 +465,7 @@ struct PCursor {
 // the previous tick's stores of that layer (fwd_fenced: forward steps fenced, counted from the
 // launch start), and a tick's backward loads (column panels holding every CTA's stores) once
 // every CTA finished the previous tick.
+template <int OPT>
 __device__ void pn_producer(const PParams& P, const PLayer* layers, const PStage* stages, float* ring,
                             uint64_t* full, uint64_t* empty, const int* fwd_fenced, int nF, const int* tbl) {
   const uint64_t pol = P.policy == 1 ? policy_evict_normal() : policy_evict_first();
@@ -484,7 +485,7 @@ __device__ void pn_producer(const PParams& P, const PLayer* layers, const PStage
         prefetch_l2(pf.L->W[pn_fbuf(P, *pf.L, t)] + pf.foff(), uint32_t(pf.ntiles()) * PN_TILE * 4u);
       } else {
         pn_tma_prefetch_3d(pf.L->tm[int(t & 1)], 0, pf.blk, pf.off);
-        if (P.adam && pn_upd(P, stages[pf.s].h, t)) {
+        if (OPT == 1 && pn_upd(P, stages[pf.s].h, t)) {
           const size_t o = (size_t(pf.blk) * pf.L->R + pf.off) * PN_TILE;
           prefetch_l2(pf.L->mW + o, uint32_t(pf.ntiles()) * PN_TILE * 4u);
           prefetch_l2(pf.L->vW + o, uint32_t(pf.ntiles()) * PN_TILE * 4u);
@@ -532,7 +533,7 @@ __device__ void pn_producer(const PParams& P, const PLayer* layers, const PStage
       }
     }
     // an updating Adam backward chunk loads W, m and v into three consecutive ring slots
-    const int nparts = (P.adam && !cur.fwd() && pn_upd(P, stages[cur.s].h, t)) ? 3 : 1;
+    const int nparts = (OPT == 1 && !cur.fwd() && pn_upd(P, stages[cur.s].h, t)) ? 3 : 1;
     for (int part = 0; part < nparts && !dead; ++part) {
       const int slot = int(chunk % uint32_t(nslot));
       const uint32_t use = chunk / uint32_t(nslot);
@@ -907,7 +908,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constan
           tma_prefetch_desc(s_layers[l].tm[b]);
 
         }
-      pn_producer(P, s_layers, s_stages, sm.ring, sm.full, sm.empty, sm.flags, nF, sm.blk);
+      pn_producer<OPT>(P, s_layers, s_stages, sm.ring, sm.full, sm.empty, sm.flags, nF, sm.blk);
     }
     return;
   }
@@ -1209,7 +1210,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constan
         const bool need_gin = !(h == 1 && i == 0);  // the network's first layer publishes no g_in
         // weight chunks: every layer with a g_in, and the first layer when it updates in the
         // backward (Adam); SGD defers the first layer's update to the next forward (L.bw == 0)
-        const bool do_chunks = need_gin || L.bw;
+        const bool do_chunks = need_gin || (OPT == 1 && L.bw);
         const bool stage_last = i == S.k - 1;
         const bool loss_src = stage_last && h == P.D;
         PN_TR(11);
@@ -1357,7 +1358,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constan
               __syncwarp();
               if (lane == 0) mbar_arrive(&sm.empty[slot]);
             }
-            if (!need_gin) continue;  // the network's first layer (Adam): update only
+            if (OPT == 1 && !need_gin) continue;  // the network's first layer (Adam): update only
             // column sums over tr (lane bits 2-4, warp bit 0) and tg (warp bits 1-2)
             float g[4] = {acc.x, acc.y, acc.z, acc.w};
 #pragma unroll

@@ -13,6 +13,7 @@ from paper_2210_09147_b200 import engine, model as mdl, streams  # noqa: E402
 
 CASES = {"tile": ([256, 512, 512, 256, 256], 16), "tick": ([32, 64, 64, 64, 16], 1),
          "panel": ([32, 64, 64, 64, 16], 1), "panel_wide": ([256, 512, 512, 512, 128], 1),
+         "panel_adam": ([256, 512, 512, 512, 128], 1), "tile_adam": ([256, 512, 512, 256, 256], 16),
          "tick_mb": ([64, 96, 96, 96, 32], 4), "tick_conc": ([256] * 9, 1), "tick_conc_mb": ([128] * 9, 4),
          "tick_mb_wide": ([1218, 3805, 2590, 1500], 2)}
 
@@ -28,7 +29,9 @@ def main(kind, counts, learn):
     s0 = (lambda a: a[0]) if M > 1 else (lambda a: a[0, 0])
 
     def run():
-        p = engine.Pipeline(mdl.mlp(widths, seed=4), counts, "sgd", 0.05, s0(xs), s0(ys), learn=learn)
+        opt = "adam" if kind.endswith("_adam") else "sgd"
+        p = engine.Pipeline(mdl.mlp(widths, seed=4), counts, opt, 0.05 if opt == "sgd" else 1e-3, s0(xs), s0(ys),
+                            learn=learn)
         assert p.kernel_path == kind.split("_")[0], p.kernel_path
         o, l, _ = p.run(xs, ys)
         W = [p.get_layer(j)[0] for j in range(p.L)]

@@ -19,6 +19,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 @pytest.mark.parametrize("kind,counts,learn", [("tile", "7", "0"), ("tile", "7", "1"), ("tile", "4,3", "1"),
                                                ("tick", "4,3", "1"), ("tick_mb", "4,3", "1"),
                                                ("panel", "4,3", "1"), ("panel", "7", "0"), ("panel_wide", "2,2,3", "1"),
+                                               ("panel_adam", "4,3", "1"), ("tile_adam", "4,3", "1"),
                                                ("tick_conc", "8,7", "1"), ("tick_conc", "4,4,4,3", "1"),
                                                ("tick_conc_mb", "6,4,5", "1"), ("tick_mb_wide", "2,2,1", "1")])
 def test_jitter_bitwise(kind, counts, learn):
