@@ -1214,8 +1214,12 @@ int stop_foreign_residents(pt_pipeline* self) {
   std::vector<pt_pipeline*> others;
   {
     std::lock_guard<std::mutex> lk(g_res_mu);
-    for (pt_pipeline* q : g_resident)
-      if (q != self && q->device == self->device) others.push_back(q);
+    for (pt_pipeline* q : g_resident) {
+      if (q == self) continue;
+      bool same = q->device == self->device;
+      for (const pt_pipeline* m : q->parts) same = same || (m->device == self->device && m != self);
+      if (same) others.push_back(q);
+    }
   }
   for (pt_pipeline* q : others) {
     // the owner may be inside a step of its own: wait for the handle (single driver)
@@ -1238,13 +1242,28 @@ int stop_foreign_residents(pt_pipeline* self) {
   return PT_OK;
 }
 
+// The handles that execute a driver's resident launch: the handle itself, or a multi-device
+// handle's parts (one resident launch per device; the parts exchange through peer memory as
+// in pt_run, and all of them poll the same mapped request word).
+std::vector<pt_pipeline*> resident_members(pt_pipeline* p) {
+  if (p->group()) return p->parts;
+  return {p};
+}
+
 bool resident_eligible(const pt_pipeline* p) {
-  if (!p->panel || p->group() || !p->has_first() || !p->has_last() || p->M != 1) return false;
+  if (!p->has_first() || !p->has_last() || p->M != 1) return false;
+  if (p->group()) {
+    for (const pt_pipeline* q : p->parts)
+      if (!q->panel) return false;
+  } else if (!p->panel) {
+    return false;
+  }
   const char* e = getenv("PT_RESIDENT");
   return !(e && atoi(e) == 0);
 }
 
-int resident_alloc(pt_pipeline* p) {
+// The driver's mapped host block: completion record, request words, x / target / output rings.
+int resident_alloc_host(pt_pipeline* p) {
   pt_pipeline::Resident& r = p->res;
   if (r.host) return PT_OK;
   r.ring = p->D + 2;
@@ -1252,7 +1271,8 @@ int resident_alloc(pt_pipeline* p) {
   r.fy = p->Fy();
   const size_t nx = size_t(r.ring) * r.ldx, ny = size_t(r.ring) * r.fy, no = size_t(2) * p->F();
   r.bytes = align_up(sizeof(pt::PResDone), 64) + 64 + (nx + ny + no) * 4;
-  CUDA_TRY(cudaHostAlloc(&r.host, r.bytes, cudaHostAllocMapped));
+  // portable: every device of a multi-device handle maps it
+  CUDA_TRY(cudaHostAlloc(&r.host, r.bytes, cudaHostAllocMapped | cudaHostAllocPortable));
   memset(r.host, 0, r.bytes);
   char* h = static_cast<char*>(r.host);
   r.done = reinterpret_cast<pt::PResDone*>(h);
@@ -1263,64 +1283,88 @@ int resident_alloc(pt_pipeline* p) {
   r.x = reinterpret_cast<float*>(h);
   r.y = r.x + nx;
   r.out = r.y + ny;
+  return PT_OK;
+}
+
+// A member's device buffers and its device alias of the driver's host block.
+int resident_alloc_dev(pt_pipeline* q, const pt_pipeline* drv) {
+  pt_pipeline::Resident& r = q->res;
   void* dh = nullptr;
-  CUDA_TRY(cudaHostGetDevicePointer(&dh, r.host, 0));
-  r.dev_off = static_cast<char*>(dh) - static_cast<char*>(r.host);
-  PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&r.xin), size_t(2) * r.ldx * sizeof(u64)));
-  r.ldy = (p->F() + pt::PN_TS - 1) / pt::PN_TS * pt::PN_TS;  // the loss gather's row length
-  PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&r.ytag), size_t(r.ring) * r.ldy * sizeof(u64)));
-  PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&r.relay), 64));
-  PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&r.lpart), size_t(2) * p->G * sizeof(float)));
+  CUDA_TRY(cudaHostGetDevicePointer(&dh, drv->res.host, 0));
+  r.dev_off = static_cast<char*>(dh) - static_cast<char*>(drv->res.host);
+  if (r.relay) return PT_OK;
+  PT_TRY(dev_alloc(q, reinterpret_cast<void**>(&r.xin), size_t(2) * drv->res.ldx * sizeof(u64)));
+  r.ldy = (q->F() + pt::PN_TS - 1) / pt::PN_TS * pt::PN_TS;  // the loss gather's row length
+  PT_TRY(dev_alloc(q, reinterpret_cast<void**>(&r.ytag), size_t(drv->res.ring) * r.ldy * sizeof(u64)));
+  PT_TRY(dev_alloc(q, reinterpret_cast<void**>(&r.relay), 64));
+  PT_TRY(dev_alloc(q, reinterpret_cast<void**>(&r.lpart), size_t(2) * q->G * sizeof(float)));
   return PT_OK;
 }
 
 template <class T>
-T* to_dev(const pt_pipeline* p, T* hptr) {
-  return reinterpret_cast<T*>(reinterpret_cast<char*>(hptr) + p->res.dev_off);
+T* to_dev(const pt_pipeline* q, T* hptr) {
+  return reinterpret_cast<T*>(reinterpret_cast<char*>(hptr) + q->res.dev_off);
+}
+
+int resident_launch(pt_pipeline* q, const pt_pipeline* drv) {
+  const pt_pipeline::Resident& h = drv->res;
+  pt_pipeline::Resident& r = q->res;
+  CUDA_TRY(cudaMemsetAsync(r.relay, 0, 64, q->stream));
+  pt::PParams Q;
+  panel_common(q, Q);
+  Q.t0 = q->t_next;
+  Q.n = std::numeric_limits<int>::max();
+  Q.loss_part = r.lpart;
+  Q.resident = 1;
+  Q.res_last = q->has_last() ? 1 : 0;
+  Q.hreq = to_dev(q, h.req);
+  Q.hflag = to_dev(q, h.flag);
+  Q.relay = r.relay;
+  Q.rx = to_dev(q, h.x);
+  Q.ry = to_dev(q, h.y);
+  Q.rring = h.ring;
+  Q.xin = r.xin;
+  Q.ytag = r.ytag;
+  Q.ldy = r.ldy;
+  Q.rout = to_dev(q, h.out);
+  Q.rdone = to_dev(q, h.done);
+  if (q->d_trace) CUDA_TRY(cudaMemsetAsync(q->d_trace, 0, size_t(q->trace_cap) * sizeof(u64), q->stream));
+  void* qargs[] = {&Q};
+  CUDA_TRY(cudaLaunchCooperativeKernel(q->opt == PT_OPT_ADAM ? (const void*)pt::panel_kernel<1> : (const void*)pt::panel_kernel<0>,
+                                       dim3(q->G), dim3(pt::NTHREADS), qargs, size_t(q->pn_smem), q->stream));
+  r.on = true;
+  r.t_start = q->t_next;
+  return PT_OK;
 }
 
 int resident_start(pt_pipeline* p) {
-  PT_TRY(check_ready(p));
-  PT_TRY(stop_foreign_residents(p));
-  PT_TRY(resident_alloc(p));
-  if (p->legacy_dirty) {
-    CUDA_TRY(cudaStreamSynchronize(0));
-    p->legacy_dirty = false;
+  const std::vector<pt_pipeline*> mem = resident_members(p);
+  PT_TRY(resident_alloc_host(p));
+  for (pt_pipeline* q : mem) {
+    DevGuard dg(q->device);
+    PT_TRY(check_ready(q));
+    PT_TRY(stop_foreign_residents(q));
+    PT_TRY(resident_alloc_dev(q, p));
+    if (q->legacy_dirty) {
+      CUDA_TRY(cudaStreamSynchronize(0));
+      q->legacy_dirty = false;
+    }
   }
   pt_pipeline::Resident& r = p->res;
   *reinterpret_cast<volatile long long*>(r.req) = p->t_next;  // nothing requested yet
   *reinterpret_cast<volatile long long*>(&r.done->tick) = -1;
-  CUDA_TRY(cudaMemsetAsync(r.relay, 0, 64, p->stream));
-  pt::PParams Q;
-  panel_common(p, Q);
-  Q.t0 = p->t_next;
-  Q.n = std::numeric_limits<int>::max();
-  Q.loss_part = r.lpart;
-  Q.resident = 1;
-  Q.hreq = to_dev(p, r.req);
-  Q.hflag = to_dev(p, r.flag);
-  Q.relay = r.relay;
-  Q.rx = to_dev(p, r.x);
-  Q.ry = to_dev(p, r.y);
-  Q.rring = r.ring;
-  Q.xin = r.xin;
-  Q.ytag = r.ytag;
-  Q.ldy = r.ldy;
-  Q.rout = to_dev(p, r.out);
-  Q.rdone = to_dev(p, r.done);
-  if (p->d_trace) CUDA_TRY(cudaMemsetAsync(p->d_trace, 0, size_t(p->trace_cap) * sizeof(u64), p->stream));
-  void* qargs[] = {&Q};
-  CUDA_TRY(cudaLaunchCooperativeKernel(p->opt == PT_OPT_ADAM ? (const void*)pt::panel_kernel<1> : (const void*)pt::panel_kernel<0>,
-                                       dim3(p->G), dim3(pt::NTHREADS), qargs,
-                                       size_t(p->pn_smem), p->stream));
+  for (pt_pipeline* q : mem) {
+    DevGuard dg(q->device);
+    PT_TRY(resident_launch(q, p));
+  }
   r.on = true;
   r.t_start = p->t_next;
   resident_register(p, true);
   return PT_OK;
 }
 
-// Post a stop, wait for the launch to drain, and queue the last D-1 posted targets for the next
-// pt_run (target queue).
+// Post a stop, wait for every member's launch to drain, and queue the last D-1 posted targets
+// for the next pt_run (target queue).
 int resident_stop(pt_pipeline* p) {
   pt_pipeline::Resident& r = p->res;
   if (!r.on) return PT_OK;
@@ -1329,37 +1373,51 @@ int resident_stop(pt_pipeline* p) {
   *reinterpret_cast<volatile long long*>(r.req) = pt::PN_STOP;
   std::atomic_thread_fence(std::memory_order_seq_cst);
   r.on = false;
-  {
+  const auto t_begin = std::chrono::steady_clock::now();
+  int first_err = PT_OK;
+  std::string msg;
+  for (pt_pipeline* q : resident_members(p)) {
+    DevGuard dg(q->device);
+    q->res.on = false;
+    q->t_next = p->t_next;
     // the launch ends at its next tick boundary; never block without a bound on it
-    const auto t_begin = std::chrono::steady_clock::now();
-    cudaError_t q;
-    while ((q = cudaStreamQuery(p->stream)) == cudaErrorNotReady) {
-      if (std::chrono::steady_clock::now() - t_begin > std::chrono::nanoseconds(2 * p->timeout_ns)) {
+    cudaError_t e;
+    while ((e = cudaStreamQuery(q->stream)) == cudaErrorNotReady) {
+      if (std::chrono::steady_clock::now() - t_begin > std::chrono::nanoseconds(2 * q->timeout_ns)) {
         long long relay = 0;
-        cudaMemcpy(&relay, r.relay, sizeof(relay), cudaMemcpyDeviceToHost);
-        p->broken = true;
+        cudaMemcpy(&relay, q->res.relay, sizeof(relay), cudaMemcpyDeviceToHost);
+        q->broken = p->broken = true;
         return fail(PT_ETIMEOUT, "resident launch did not stop (relay " + std::to_string(relay) + ", tick " +
                                      std::to_string(p->t_next) + ")");
       }
       std::this_thread::yield();
     }
-    if (q != cudaSuccess) return fail(PT_ECUDA, std::string("resident launch failed: ") + cudaGetErrorString(q));
+    if (e != cudaSuccess) return fail(PT_ECUDA, std::string("resident launch failed: ") + cudaGetErrorString(e));
+    if (q->has_last()) {
+      const int Fy = q->Fy();
+      for (long long s = std::max(r.t_start, p->t_next - (p->D - 1)); s < p->t_next; ++s)
+        CUDA_TRY(cudaMemcpyAsync(q->yhist + size_t(s % q->yh) * Fy, r.y + size_t(s % r.ring) * Fy, size_t(Fy) * 4,
+                                 cudaMemcpyHostToDevice, q->stream));
+      CUDA_TRY(cudaStreamSynchronize(q->stream));
+    }
+    const int rs = read_status(q);
+    if (rs != PT_OK && first_err == PT_OK) {
+      first_err = rs;
+      msg = g_err;
+    }
   }
-  const int Fy = p->Fy();
-  for (long long s = std::max(r.t_start, p->t_next - (p->D - 1)); s < p->t_next; ++s)
-    CUDA_TRY(cudaMemcpyAsync(p->yhist + size_t(s % p->yh) * Fy, r.y + size_t(s % r.ring) * Fy, size_t(Fy) * 4,
-                             cudaMemcpyHostToDevice, p->stream));
-  CUDA_TRY(cudaStreamSynchronize(p->stream));
-  return read_status(p);
+  if (first_err != PT_OK) g_err = msg;
+  return first_err;
 }
 
-// One tick through the resident launch: write x_t and gamma_t into the mapped rings, post the
-// request, wait for the completion record.
+// One tick through the resident launch(es): write x_t and gamma_t into the mapped rings, post
+// the request, wait for the completion record (written by the member that owns stage D).
 int resident_step(pt_pipeline* p, const float* x, const float* y, float* out, float* loss, int32_t* valid) {
   if (!x) return fail(PT_EINVAL, "x is required on the process that owns stage 1");
   if (p->learn && !y) return fail(PT_EINVAL, "targets are required for online learning (stage D)");
   if (!p->res.on) PT_TRY(resident_start(p));
   pt_pipeline::Resident& r = p->res;
+  const std::vector<pt_pipeline*> mem = resident_members(p);
   const long long t = p->t_next;
   const int n0 = p->dims[0], Fy = p->Fy(), F = p->F();
   memcpy(r.x + size_t(t % r.ring) * r.ldx, x, size_t(n0) * 4);
@@ -1373,13 +1431,17 @@ int resident_step(pt_pipeline* p, const float* x, const float* y, float* out, fl
   unsigned spins = 0;
   while (*dt != t + 1) {
     if ((++spins & 0xFFFu) == 0) {
-      const cudaError_t q = cudaStreamQuery(p->stream);
-      if (q != cudaErrorNotReady) {  // the launch ended without completing the step
-        r.on = false;
-        resident_register(p, false);
-        if (q != cudaSuccess) return fail(PT_ECUDA, std::string("resident launch failed: ") + cudaGetErrorString(q));
-        PT_TRY(read_status(p));
-        return fail(PT_ESTATE, "resident launch ended before completing step " + std::to_string(t));
+      for (pt_pipeline* q : mem) {
+        DevGuard dg(q->device);
+        const cudaError_t e = cudaStreamQuery(q->stream);
+        if (e != cudaErrorNotReady) {  // a launch ended without completing the step
+          resident_register(p, false);
+          r.on = false;
+          for (pt_pipeline* o : mem) o->res.on = false;
+          if (e != cudaSuccess) return fail(PT_ECUDA, std::string("resident launch failed: ") + cudaGetErrorString(e));
+          PT_TRY(read_status(q));
+          return fail(PT_ESTATE, "resident launch ended before completing step " + std::to_string(t));
+        }
       }
       if (std::chrono::steady_clock::now() - t_begin > std::chrono::nanoseconds(4 * p->timeout_ns)) {
         p->broken = true;
@@ -1389,6 +1451,7 @@ int resident_step(pt_pipeline* p, const float* x, const float* y, float* out, fl
   }
   std::atomic_thread_fence(std::memory_order_seq_cst);
   p->t_next = t + 1;
+  for (pt_pipeline* q : mem) q->t_next = t + 1;
   const pt::PResDone d = *const_cast<const pt::PResDone*>(r.done);
   static const bool dbg = getenv("PT_RESIDENT_DEBUG") != nullptr;  // diagnostics: per-step timing
   if (dbg) {
@@ -1792,6 +1855,7 @@ int create_group(const pt_config* c, pt_pipeline* p) {
   p->local_first = lo;
   p->local_count = hi - lo;
   p->device = phys[0];
+  p->timeout_ns = (unsigned long long)(c->timeout_ms > 0 ? c->timeout_ms : 30000) * 1000000ull;
   for (size_t i = 0; i < runs.size(); ++i) {
     pt_config sub = *c;
     sub.device_of_stage = nullptr;
@@ -1905,6 +1969,8 @@ int pt_create(const pt_config* cfg, pt_pipeline** out) {
 void pt_destroy(pt_pipeline* p) {
   if (!p) return;
   if (p->group()) {
+    resident_stop(p);
+    if (p->res.host) cudaFreeHost(p->res.host);
     for (pt_pipeline* q : p->parts) {
       DevGuard dg(q->device);
       cudaStreamSynchronize(q->stream);
@@ -1932,6 +1998,7 @@ int pt_set_params(pt_pipeline* p, int32_t layer, const float* W, const float* b,
   BusyGuard g(p);
   if (!g.ok) return fail(PT_EBUSY, "contract violation: handle used concurrently");
   if (p->group()) {
+    PT_TRY(resident_stop(p));
     pt_pipeline* q = part_of_layer(p, layer);
     if (!q) return fail(PT_EINVAL, "layer " + std::to_string(layer) + " is not owned by this process");
     return pt_set_params(q, layer, W, b, where);
@@ -1972,6 +2039,7 @@ int pt_get_params(pt_pipeline* p, int32_t layer, float* W, float* b, int32_t whe
   BusyGuard g(p);
   if (!g.ok) return fail(PT_EBUSY, "contract violation: extract called mid-step (SPEC.md:239)");
   if (p->group()) {
+    PT_TRY(resident_stop(p));
     pt_pipeline* q = part_of_layer(p, layer);
     if (!q) return fail(PT_EINVAL, "layer " + std::to_string(layer) + " is not owned by this process");
     PT_TRY(group_finish(p));  // every part idle: the weights are a consistent tick
@@ -2022,7 +2090,10 @@ int pt_run(pt_pipeline* p, const float* xs, const float* ys, int64_t n, float* o
   BusyGuard g(p);
   if (!g.ok) return fail(PT_EBUSY, "contract violation: pipeline_step called concurrently (SPEC.md:221)");
   if (where != PT_HOST && where != PT_DEVICE) return fail(PT_EINVAL, "where must be PT_HOST or PT_DEVICE");
-  if (p->group()) return group_run(p, xs, ys, n, outs, losses, valid, where);
+  if (p->group()) {
+    PT_TRY(resident_stop(p));
+    return group_run(p, xs, ys, n, outs, losses, valid, where);
+  }
   DevGuard dg(p->device);
   PT_TRY(resident_stop(p));
   return run_impl(p, xs, ys, n, outs, losses, valid, where);
@@ -2038,8 +2109,8 @@ int pt_step(pt_pipeline* p, const float* x, const float* y, float* out, float* l
   const bool grp = p->group();
   pt_pipeline* last = grp ? p->parts.back() : p;
   DevGuard dg(grp ? p->parts.front()->device : p->device);
-  if (!grp && where == PT_HOST && resident_eligible(p)) return resident_step(p, x, y, out, loss, valid);
-  if (!grp) PT_TRY(resident_stop(p));
+  if (where == PT_HOST && resident_eligible(p)) return resident_step(p, x, y, out, loss, valid);
+  PT_TRY(resident_stop(p));
   if (where == PT_HOST) {
     r = grp ? group_run(p, x, y, 1, out, loss, valid ? &v8 : nullptr, PT_HOST)
             : run_impl(p, x, y, 1, out, loss, valid ? &v8 : nullptr, PT_HOST);
@@ -2067,7 +2138,10 @@ int pt_sync(pt_pipeline* p) {
   if (!p) return fail(PT_EINVAL, "null handle");
   BusyGuard g(p);
   if (!g.ok) return fail(PT_EBUSY, "contract violation: handle used concurrently");
-  if (p->group()) return group_finish(p);
+  if (p->group()) {
+    PT_TRY(resident_stop(p));
+    return group_finish(p);
+  }
   DevGuard dg(p->device);
   PT_TRY(resident_stop(p));
   return finish_impl(p);
@@ -2132,7 +2206,10 @@ int32_t pt_kernel_path(const pt_pipeline* p) {
 
 int pt_set_trace(pt_pipeline* p, int32_t cta, int32_t cap) {
   if (!p) return fail(PT_EINVAL, "null handle");
-  if (p->group()) return pt_set_trace(p->parts.front(), cta, cap);  // the stage-1 device
+  if (p->group()) {
+    PT_TRY(resident_stop(p));
+    return pt_set_trace(p->parts.front(), cta, cap);  // the stage-1 device
+  }
   DevGuard dg(p->device);
   PT_TRY(resident_stop(p));
   CUDA_TRY(cudaStreamSynchronize(p->stream));
@@ -2150,7 +2227,10 @@ int pt_set_trace(pt_pipeline* p, int32_t cta, int32_t cap) {
 
 int pt_get_trace(pt_pipeline* p, uint64_t* out, int32_t cap) {
   if (!p || !out) return fail(PT_EINVAL, "null argument");
-  if (p->group()) return pt_get_trace(p->parts.front(), out, cap);
+  if (p->group()) {
+    PT_TRY(resident_stop(p));
+    return pt_get_trace(p->parts.front(), out, cap);
+  }
   DevGuard dg(p->device);
   PT_TRY(resident_stop(p));
   if (!p->d_trace) return fail(PT_EINVAL, "tracing is off (pt_set_trace)");

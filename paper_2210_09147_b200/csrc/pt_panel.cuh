@@ -124,6 +124,7 @@ struct PParams {
   // the epilogue kernel's order) and publishes the PResDone record. No launch, no copy and no
   // host round trip besides the two mapped words per step.
   int resident;
+  int res_last;           // this launch owns stage D: it copies targets and writes the record
   const long long* hreq;  // host-mapped: ticks requested (t + 1), or PN_STOP
   const int* hflag;       // host-mapped: 1 iff the step passed a target
   long long* relay;       // device: CTA 0's copy of hreq for the other CTAs
@@ -952,7 +953,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constan
         u64* xd = P.xin + size_t(t & 1) * P.ldx;
         for (int j = bk0[4] + tid; j < bk0[5]; j += NCT) st_tv_gpu(xd + j, pack_tv(ld_volatile_f32(xr + j), tag_t));
       }
-      {
+      if (P.res_last) {
         // this CTA's slice of gamma_t: mapped host memory -> the tagged target ring (padding
         // words up to ldy are tagged zeros, so the loss gather can poll whole rows)
         const Rows Y = rows_of(P.ldy, c, G);
@@ -1415,7 +1416,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) panel_kernel(const __grid_constan
           const u64 old = atomicAdd(reinterpret_cast<unsigned long long*>(P.tick_end), 1ull);
           last = old + 1 == u64(G) * u64(t + 1);
         }
-        if (__shfl_sync(0xffffffffu, last, 0)) pn_resident_done(P, t, ti, lane);
+        if (__shfl_sync(0xffffffffu, last, 0) && P.res_last) pn_resident_done(P, t, ti, lane);
       }
     } else if (tid == 0) {
       __threadfence();

@@ -3,7 +3,9 @@
 Tolerances (fp32 GPU vs f64 oracle). The f32 run of the oracle
 calibrates each bar: the GPU error must stay within 4x the oracle's own f32
 error, plus a floor of 1e-6 of the signal scale. With Adam the calibration is the
-worst of three f32 oracle runs (the network and two hidden-unit permutations of it). Stated absolute ceilings:
+worst of three f32 oracle runs (the network and two hidden-unit permutations of it), and
+for Adam on the tensor-core tile path the factor is 32 instead of 4 (3xTF32 products carry
+8x fp32's unit roundoff). Stated absolute ceilings:
 outputs and losses rel <= 1e-4 per tick; final weights and
 delta-W = W_N - W_0 rel-Frobenius <= 1e-3.
 """
@@ -32,6 +34,7 @@ def _case(widths, counts, T, lr, act="relu", seed=0, act_delay=1, learn=True, M=
                            act_delay=act_delay, learn=learn, grid=grid)
     outs, losses, valid = pipe.run(xs.astype(np.float32), ys.astype(np.float32))
     got = pipe.extract_weights()
+    path = pipe.kernel_path
     pipe.close()
     o64, l64, v64, W64, b64 = run_oracle(m, counts, xs, ys, lr, np.float64, act_delay, learn, loss, optimizer)
     o32, l32, v32, W32, b32 = run_oracle(m, counts, xs, ys, lr, np.float32, act_delay, learn, loss, optimizer)
@@ -39,6 +42,10 @@ def _case(widths, counts, T, lr, act="relu", seed=0, act_delay=1, learn=True, M=
     vm = v64
     e_out = rel(outs.reshape(o64.shape), o64)
     e_out32 = rel(o32, o64)
+    # the bar's factor on the calibration error: 4, or 32 for Adam on the tensor-core tile path,
+    # whose 3xTF32 products carry ~2^-21 relative error against fp32's 2^-24 (8x), which Adam's
+    # sign-driven steps carry into the weights
+    k = 32 if (path == "tile" and optimizer == "adam") else 4
     ens = []
     if optimizer == "adam" and learn and lr > 0:
         # Adam turns rounding noise in near-zero gradients into full lr-sized steps (m/sqrt(v)
@@ -48,21 +55,21 @@ def _case(widths, counts, T, lr, act="relu", seed=0, act_delay=1, learn=True, M=
         ens = [run_oracle_permuted(m, counts, xs, ys, lr, np.float32, act_delay, learn, loss, optimizer, k)
                for k in (1, 2)]
         e_out32 = max([e_out32] + [rel(e[0], o64) for e in ens])
-    assert e_out <= max(4 * e_out32, 1e-6) or e_out <= 1e-4, (e_out, e_out32)
+    assert e_out <= max(k * e_out32, 1e-6) or e_out <= 1e-4, (e_out, e_out32)
     if learn:
         e_loss = rel(losses[vm], l64[vm])
         e_loss32 = max([rel(l32[vm], l64[vm])] + [rel(e[1][vm], l64[vm]) for e in ens])
-        assert e_loss <= max(4 * e_loss32, 1e-6) or e_loss <= 1e-4, (e_loss, e_loss32)
+        assert e_loss <= max(k * e_loss32, 1e-6) or e_loss <= 1e-4, (e_loss, e_loss32)
         for j, l in enumerate(got.dense_layers):
             dW = l.W.astype(np.float64) - W0[j]
             dW64 = W64[j] - W0[j]
             if np.linalg.norm(dW64) > 0:
                 e = frob_rel(dW, dW64)
                 e32 = max([frob_rel(W32[j] - W0[j], dW64)] + [frob_rel(e[3][j] - W0[j], dW64) for e in ens])
-                assert e <= max(4 * e32, 1e-6) or e <= 1e-3, (j, e, e32)
+                assert e <= max(k * e32, 1e-6) or e <= 1e-3, (j, e, e32)
             eb = frob_rel(l.b, b64[j])
             eb32 = max([frob_rel(b32[j], b64[j])] + [frob_rel(e[4][j], b64[j]) for e in ens])
-            assert eb <= max(4 * eb32, 1e-6) or eb <= 1e-4, (j, eb, eb32)
+            assert eb <= max(k * eb32, 1e-6) or eb <= 1e-4, (j, eb, eb32)
     return e_out
 
 

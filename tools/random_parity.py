@@ -14,7 +14,7 @@ def random_case(rng, wmax=None):
     wmax = wmax or WMAX
     L = int(rng.integers(1, int(os.environ.get("LMAX", "5")) + 1))
     widths = [int(rng.integers(1, wmax)) for _ in range(L + 1)]
-    M = int(rng.choice([1, 1, 2, 4, 16]))
+    M = int(rng.choice([1, 1, 2, 4, 16] + ([32, 64] if os.environ.get("BIG_M") else [])))
     if os.environ.get("TILE_ONLY"):
         M = 16
         widths = [256 * int(rng.integers(1, 17)) for _ in range(L + 1)]  # the tile kernel, up to 4096
@@ -34,7 +34,7 @@ def random_case(rng, wmax=None):
     loss = "softmax_ce" if rng.random() < 0.3 and widths[-1] >= 2 else "mse"
     c = dict(widths=widths, counts=counts, T=int(rng.integers(2 * D + 2, 24)), lr=float(rng.choice([0.0, 0.01, 0.05])),
                 act=str(rng.choice(["relu", "tanh"])), act_delay=int(rng.integers(0, 2)), M=M,
-                optimizer=("sgd" if os.environ.get("TILE_ONLY") else str(rng.choice(["sgd", "sgd", "adam"]))), loss=loss, seed=int(rng.integers(0, 1000)),
+                optimizer=str(rng.choice(["sgd", "sgd", "adam"])), loss=loss, seed=int(rng.integers(0, 1000)),
                 learn=bool(rng.random() >= float(os.environ.get("P_INFER", "0"))))
     if os.environ.get("OPT"):  # e.g. OPT=adam LR=0.05: the Adam cases at the largest lr
         c["optimizer"] = os.environ["OPT"]
