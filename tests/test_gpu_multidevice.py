@@ -106,6 +106,38 @@ def test_virtual_devices_step_api(virtual_devices):
     one.close()
 
 
+def test_virtual_devices_resident_steps_interleaved(virtual_devices):
+    """Per-sample steps on a multi-device handle run as one resident launch per part (all parts
+    poll the same mapped request word); runs and weight reads in between stop and restart them.
+    The result equals one pt_run on the single-device pipeline, bit for bit."""
+    import torch
+    widths, counts, T = [48, 80, 80, 80, 10], [2, 2, 3], 24
+    m = mdl.mlp(widths, seed=7)
+    xs, ys = _data(widths, T, 1, seed=8)
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    multi = engine.Pipeline(m, counts, "sgd", 0.05, xs[0, 0], ys[0, 0], devices=[0, 1, 2], timeout_ms=60000)
+    one = engine.Pipeline(m, counts, "sgd", 0.05, xs[0, 0], ys[0, 0], grid=sms // 3)
+    o_ref, l_ref, _ = one.run(xs, ys)
+    outs, t = [], 0
+    for seg, kind in ((6, "step"), (5, "run"), (4, "step"), (0, "get"), (9, "step")):
+        if kind == "get":
+            W, b = multi.get_layer(2)
+            multi.set_layer(2, W, b)
+        elif kind == "run":
+            o, _, _ = multi.run(xs[t:t + seg], ys[t:t + seg])
+            outs += list(o[:, 0])
+        else:
+            for k in range(seg):
+                outs.append(multi.step(xs[t + k, 0], ys[t + k, 0]).output)
+        t += seg
+    assert t == T
+    assert np.array_equal(np.array(outs), o_ref[:, 0])
+    for j in range(one.L):
+        assert all(np.array_equal(u, v) for u, v in zip(multi.get_layer(j), one.get_layer(j)))
+    multi.close()
+    one.close()
+
+
 def test_paper_api_devices_list(virtual_devices):
     """partime.pipeline.Pipeline(net, ..., devices=[cuda:0, cuda:1]) (PAPER.md:654)."""
     import torch
