@@ -610,3 +610,30 @@ def test_generic_multichunk_partials(M, act_delay):
     its g_in partial is a running sum over chunks and must carry the tick's tag only once
     the last chunk is in (earlier running sums were readable too soon)."""
     _case([1218, 3805, 2590, 1500], [2, 2, 1], 10, 0.05, act_delay=act_delay, M=M)
+
+
+def test_pipestream_names_end_to_end():
+    """A reference user's program, written against the `pipestream` import names only
+    (SPEC.md:208-243): build a model from LayerSpecs, run a drift2d stream with pipeline_run
+    (RunReport CSV), step per sample, extract the weights; the outputs match the oracle."""
+    from pipestream.engine import pipeline_build, pipeline_extract_weights, pipeline_run, pipeline_step
+    from pipestream.netcore import LayerSpec, Model, init_weights
+    from pipestream.streams import Drift2dStream
+    layers = [LayerSpec("dense", 2, 32), LayerSpec("relu"), LayerSpec("dense", 32, 32), LayerSpec("tanh"),
+              LayerSpec("dense", 32, 4)]
+    m = Model(layers=layers, loss="softmax_cross_entropy", input_shape=(2,), output_dim=4)
+    init_weights(m, seed=5)
+    stream = Drift2dStream(4, rho=0.01, sigma=0.1, seed=2)
+    xs, ys = stream.block(0, 40)
+    p = pipeline_build(m, [2, 3], "sgd", 0.05, xs[0, 0], ys[0, 0])
+    rows = []
+    rep = pipeline_run(p, Drift2dStream(4, rho=0.01, sigma=0.1, seed=2), 30, log_sink=rows.append)
+    assert rows[0] == "step,sample_id,loss,valid,step_wall_seconds" and len(rows) == 31
+    assert rep.valid_outputs == 29
+    outs = [pipeline_step(p, xs[t, 0], ys[t, 0]).output for t in range(30, 40)]
+    W = pipeline_extract_weights(p)
+    o64, _, _, W64, _ = run_oracle(m, [2, 3], xs, ys, 0.05, np.float64, 1, True, "softmax_ce", "sgd")
+    assert rel(np.concatenate([rep.outputs[:, 0], np.array(outs)]), o64[:, 0]) <= 1e-4
+    for j, l in enumerate(W.dense_layers):
+        assert frob_rel(l.W, W64[j]) <= 1e-4
+    p.close()

@@ -70,6 +70,8 @@ def test_c4_tile_d8_adam_ce():
     _case(w, counts, 10, 1e-4, M=16, optimizer="adam", loss="softmax_ce")  # valid outputs from t = D - 1 = 7
 
 
-def test_c5_uneven_d8():
-    """Config 5: uneven widths 1024..8192, DP-balanced stages, D = 8, 8 ticks."""
-    _case(C5, _bench_counts(C5, 8, True), 8, 1e-3)
+@pytest.mark.parametrize("D", [2, 4, 8])
+def test_c5_uneven(D):
+    """Config 5: uneven widths 1024..8192, DP-balanced stages (the scale proxy's plans),
+    D = 2 / 4 / 8, 2D + 2 ticks."""
+    _case(C5, _bench_counts(C5, D, True), 2 * D + 2, 1e-3)
