@@ -33,6 +33,10 @@ if __name__ == "__main__":
     for n in (1, 2, 4, 8):
         L = 32 // n
         cp.probe(f"C2 stage share at N={n} ({L} layers)", [2048] * (L + 1), 1, ticks=64)
+    # C3 at D=8: 8 inference layers of 4096 per GPU; C4 at D=8: 4 learning layers of 4096,
+    # micro-batch 16 (tile kernel)
+    cp.probe("C3 stage share at N=8 (8 x 4096, inference)", [4096] * 9, 1, learn=False, ticks=32)
+    cp.probe("C4 stage share at N=8 (4 x 4096, M=16)", [4096] * 5, 1, M=16, ticks=16)
     import bench
     c5 = [1024, 2048, 4096, 8192, 8192, 4096, 2048, 1024] * 3 + [1024]
     for D in (2, 4, 8):
