@@ -591,9 +591,10 @@ int setup_tile(pt_pipeline* p) {
   PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&p->d_tmaps), maps.size() * sizeof(CUtensorMap)));
   for (size_t i = 0; i < p->layers.size(); ++i) {
     const LayerHost& Lh = p->layers[i];
-    if (pt::tc_make_tmap_2d(&maps[2 * i], Lh.W, Lh.n_in, Lh.n_out, 32, 128, CU_TENSOR_MAP_SWIZZLE_128B, Lh.ld_in) ||
-        pt::tc_make_tmap_2d(&maps[2 * i + 1], Lh.W, Lh.n_in, Lh.n_out, 32, 64, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
-                            Lh.ld_in))
+    // blocked weights [n_out/128][n_in/64][128][64] (pt_tile.cuh tl_to_blocks)
+    if (pt::tc_make_tmap_blocked(&maps[2 * i], Lh.W, Lh.n_in, Lh.n_out, 32, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        pt::tc_make_tmap_blocked(&maps[2 * i + 1], Lh.W, Lh.n_in, Lh.n_out, 32, 64,
+                                 CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
       return fail(PT_ECUDA, "cuTensorMapEncodeTiled failed for layer " + std::to_string(p->layer_base + i));
     tl[i].tmf = p->d_tmaps + 2 * i;
     tl[i].tmb = p->d_tmaps + 2 * i + 1;
@@ -884,7 +885,8 @@ int create_impl(const pt_config* c, pt_pipeline* p) {
     // stage kernel waiting for a neighbour (another handle, part or process) that is itself
     // blocked in such a load would only end at the watchdog.
     const void* others[] = {(const void*)pt::panel_kernel<0>, (const void*)pt::panel_kernel<1>,
-                            (const void*)pt::tile_kernel<0>,
+                            (const void*)pt::tile_kernel<0>, (const void*)pt::tl_to_blocks,
+                            (const void*)pt::tl_from_blocks,
                             (const void*)pt::tile_kernel<1>,
                             (const void*)pt::epilogue_kernel, (const void*)pt::pn_to_tiles,
                             (const void*)pt::pn_from_tiles};
@@ -2026,6 +2028,19 @@ int pt_set_params(pt_pipeline* p, int32_t layer, const float* W, const float* b,
     CUDA_TRY(cudaStreamSynchronize(p->stream));
     return W ? upload_panel_desc(p) : PT_OK;
   }
+  if (p->tile) {
+    // row-major staging -> the tile kernel's blocked layout
+    if (W) {
+      const size_t nw = size_t(Lh->n_out) * Lh->n_in;
+      PT_TRY(panel_rowbuf(p, nw));
+      CUDA_TRY(cudaMemcpyAsync(p->rowbuf, W, nw * 4, k, p->stream));
+      pt::tl_to_blocks<<<592, 256, 0, p->stream>>>(p->rowbuf, Lh->W, Lh->n_out, Lh->n_in);
+      CUDA_TRY(cudaGetLastError());
+    }
+    if (b) CUDA_TRY(cudaMemcpyAsync(Lh->b, b, size_t(Lh->n_out) * 4, k, p->stream));
+    CUDA_TRY(cudaStreamSynchronize(p->stream));
+    return PT_OK;
+  }
   if (W)
     CUDA_TRY(cudaMemcpy2D(Lh->W, size_t(Lh->ld_in) * 4, W, size_t(Lh->n_in) * 4, size_t(Lh->n_in) * 4,
                           size_t(Lh->n_out), k));
@@ -2070,6 +2085,18 @@ int pt_get_params(pt_pipeline* p, int32_t layer, float* W, float* b, int32_t whe
       PT_TRY(panel_rowbuf(p, nw));
       pt::pn_from_tiles<<<592, 256, 0, p->stream>>>(Lh->Wt[panel_cur(p, *Lh)], p->rowbuf, Lh->n_out, Lh->n_in, Lh->C, sdel,
                                                     ahat, p->lr);
+      CUDA_TRY(cudaGetLastError());
+      CUDA_TRY(cudaMemcpyAsync(W, p->rowbuf, nw * 4, k, p->stream));
+    }
+    if (b) CUDA_TRY(cudaMemcpyAsync(b, Lh->b, size_t(Lh->n_out) * 4, k, p->stream));
+    CUDA_TRY(cudaStreamSynchronize(p->stream));
+    return PT_OK;
+  }
+  if (p->tile) {
+    if (W) {
+      const size_t nw = size_t(Lh->n_out) * Lh->n_in;
+      PT_TRY(panel_rowbuf(p, nw));
+      pt::tl_from_blocks<<<592, 256, 0, p->stream>>>(Lh->W, p->rowbuf, Lh->n_out, Lh->n_in);
       CUDA_TRY(cudaGetLastError());
       CUDA_TRY(cudaMemcpyAsync(W, p->rowbuf, nw * 4, k, p->stream));
     }

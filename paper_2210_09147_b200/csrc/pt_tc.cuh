@@ -170,6 +170,21 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* tm, const void* 
                "r"(c1), "r"(smem_u32(src))
                : "memory");
 }
+// 4-D tensor copies over the tile kernel's blocked weights [rb][cb][128][64]: coordinates
+// {column in block, row in block, column block, row block}
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* tm, int c0, int c1, int c2, int c3,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
+      "%5}], [%6];" ::"r"(smem_u32(dst)),
+      "l"(tm), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap* tm, const void* src, int c0, int c1, int c2, int c3) {
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(tm),
+               "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(src))
+               : "memory");
+}
 // A tensor map in global memory written by the host (cudaMemcpy) must be acquired by the
 // async proxy before TMA uses it: a new handle can reuse the address of a freed handle's map,
 // and a stale descriptor-cache entry would point the copies at the old weights.
@@ -201,6 +216,29 @@ static inline int tc_make_tmap_2d(CUtensorMap* tm, const float* base, int cols, 
   const cuuint32_t box[2] = {cuuint32_t(box_cols), cuuint32_t(box_rows)};
   const cuuint32_t es[2] = {1, 1};
   CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : int(r);
+}
+
+// 4-D map over blocked weights [rows/128][cols/64][128][64] fp32 (each 128 x 64 block is
+// 32 KB contiguous, so a box of whole rows of one block stays in one DRAM-contiguous region);
+// box {box_cols, box_rows, 1, 1}; 0 = ok
+static inline int tc_make_tmap_blocked(CUtensorMap* tm, const float* base, int cols, int rows, int box_cols,
+                                       int box_rows, CUtensorMapSwizzle swz) {
+  static PFN_encodeTiled fn = nullptr;
+  if (fn == nullptr) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess || p == nullptr)
+      return -1;
+    fn = reinterpret_cast<PFN_encodeTiled>(p);
+  }
+  const cuuint64_t dims[4] = {64, 128, cuuint64_t(cols / 64), cuuint64_t(rows / 128)};
+  const cuuint64_t strides[3] = {64 * 4, 128 * 64 * 4, cuuint64_t(cols / 64) * 128 * 64 * 4};
+  const cuuint32_t box[4] = {cuuint32_t(box_cols), cuuint32_t(box_rows), 1, 1};
+  const cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(base), dims, strides, box, es,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? 0 : int(r);

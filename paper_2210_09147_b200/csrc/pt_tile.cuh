@@ -279,7 +279,10 @@ __device__ void t_producer(const TParams& P, const TSmem& sm) {
     release(s);
     const CUtensorMap* tm = P.layers[pend_l[s]].tmb;
     float* base = sm.ring + size_t(s) * T_SLOT_FLOATS;
-    for (int b = 0; b < 4; ++b) tma_store_2d(tm, base + b * 2048, pend_c[s] + 32 * b, pend_r[s]);
+    for (int b = 0; b < 4; ++b) {
+      const int cc = pend_c[s] + 32 * b, rr = pend_r[s];
+      tma_store_4d(tm, base + b * 2048, cc & 63, rr & 127, cc >> 6, rr >> 7);
+    }
     pend[s] = false;
   };
   for (int ti = 0; ti < P.n && !dead; ++ti) {
@@ -318,11 +321,15 @@ __device__ void t_producer(const TParams& P, const TSmem& sm) {
             mbar_arrive_expect_tx(&sm.full[slot], T_SLOT_FLOATS * 4);
             if (sp.fwd) {
               const int r0 = blk * 128, c0 = q * (L.n_in / T_Q) + ch * T_CK;
-              tma_load_2d(dst, L.tmf, c0, r0, &sm.full[slot]);
-              tma_load_2d(dst + 4096, L.tmf, c0 + 32, r0, &sm.full[slot]);
+              // blocked weights: coordinates {column in block, row in block, column block, row block}
+              tma_load_4d(dst, L.tmf, c0 & 63, 0, c0 >> 6, r0 >> 7, &sm.full[slot]);
+              tma_load_4d(dst + 4096, L.tmf, (c0 + 32) & 63, 0, (c0 + 32) >> 6, r0 >> 7, &sm.full[slot]);
             } else {
               const int c0 = blk * 128, r0 = q * (L.n_out / T_Q) + ch * T_CK;
-              for (int b = 0; b < 4; ++b) tma_load_2d(dst + b * 2048, L.tmb, c0 + 32 * b, r0, &sm.full[slot]);
+              for (int b = 0; b < 4; ++b) {
+                const int cc = c0 + 32 * b;
+                tma_load_4d(dst + b * 2048, L.tmb, cc & 63, r0 & 127, cc >> 6, r0 >> 7, &sm.full[slot]);
+              }
               if (upd) {
                 pend[slot] = true;
                 pend_l[slot] = sp.L;
@@ -622,6 +629,23 @@ __device__ __noinline__ void t_softmax_ce(const TParams& P, const TLayer& L, con
     }
   }
   if (st_id == 0) P.loss_part[size_t(ti) * G + c] = (c == 0) ? lsum : 0.f;
+}
+
+// layout conversion of the tile kernel's blocked weights (pt_set_params / pt_get_params):
+// element (r, c) of [n_out][n_in] at ((r / 128) * (n_in / 64) + c / 64) * 8192 + (r % 128) * 64 + c % 64
+__global__ void tl_to_blocks(const float* __restrict__ src, float* __restrict__ dst, int n_out, int n_in) {
+  const size_t total = size_t(n_out) * n_in;
+  for (size_t e = blockIdx.x * size_t(blockDim.x) + threadIdx.x; e < total; e += size_t(gridDim.x) * blockDim.x) {
+    const int r = int(e / n_in), c = int(e % n_in);
+    dst[(size_t(r >> 7) * (n_in >> 6) + (c >> 6)) * 8192 + (r & 127) * 64 + (c & 63)] = src[e];
+  }
+}
+__global__ void tl_from_blocks(const float* __restrict__ src, float* __restrict__ dst, int n_out, int n_in) {
+  const size_t total = size_t(n_out) * n_in;
+  for (size_t e = blockIdx.x * size_t(blockDim.x) + threadIdx.x; e < total; e += size_t(gridDim.x) * blockDim.x) {
+    const int r = int(e / n_in), c = int(e % n_in);
+    dst[e] = src[(size_t(r >> 7) * (n_in >> 6) + (c >> 6)) * 8192 + (r & 127) * 64 + (c & 63)];
+  }
 }
 
 // OPT: 0 SGD, 1 Adam (separate instantiations: the Adam moments' registers stay out of the
