@@ -124,7 +124,10 @@ class ClockSampler:
 
 
 def cpu_reference(widths, D, ticks_budget_s, steps=None, warmup=0, ticks_per_step=None):
-    """Time the oracle (numpy f32, OpenBLAS on every host core) on the same config.
+    """Time the oracle (numpy f32 + OpenBLAS) on the same config: D = 1 gives BLAS every host
+    core; D > 1 runs BASELINE.md §3's threaded pipeline (one worker thread per stage, two
+    barriers per tick) with floor(cores / D) BLAS threads per worker
+    (`tools/cpu_scaling.py` measures D = 1, 2, 4, 8).
 
     Returns (samples/s, cores, sample description, per-step seconds).
     """
@@ -133,7 +136,7 @@ def cpu_reference(widths, D, ticks_budget_s, steps=None, warmup=0, ticks_per_ste
     cores = len(os.sched_getaffinity(0))
     try:
         from threadpoolctl import threadpool_limits
-        threadpool_limits(cores)
+        threadpool_limits(max(1, cores // D))
     except Exception:
         pass
     m = mdl.mlp(widths, seed=0, dtype=np.float32)
@@ -161,7 +164,7 @@ def cpu_reference(widths, D, ticks_budget_s, steps=None, warmup=0, ticks_per_ste
             n += 1
         el = time.perf_counter() - t0
         p.close()
-        return n / el, cores, f"{n} ticks of C2 (D={D}) in {el:.1f}s, numpy f32 + OpenBLAS", [el]
+        return n / el, cores, f"{n} ticks of C2 (D={D}) in {el:.1f}s, numpy f32 + OpenBLAS ({max(1, cores // D)} threads x {D})", [el]
     for _ in range(steps):
         t0 = time.perf_counter()
         for _ in range(ticks_per_step):
@@ -170,7 +173,7 @@ def cpu_reference(widths, D, ticks_budget_s, steps=None, warmup=0, ticks_per_ste
         times.append(time.perf_counter() - t0)
     p.close()
     n = steps * ticks_per_step
-    return n / sum(times), cores, f"{ticks_per_step} ticks/step of C2 (D={D}), numpy f32 + OpenBLAS", times
+    return n / sum(times), cores, f"{ticks_per_step} ticks/step of C2 (D={D}), numpy f32 + OpenBLAS ({max(1, cores // D)} threads x {D})", times
 
 
 def run_reference(args):
