@@ -212,7 +212,7 @@ def balanced_counts(widths, D, learn):
 
 def extra_configs(peak):
     """Device time per tick of the other BASELINE.json configs on this one GPU (all stages
-    here): C3 inference wave, C4 micro-batch 16 (tcgen05 tile kernel), C5 uneven widths.
+    here): C3 inference wave, C4 micro-batch 16 and 32 (tcgen05 tile kernel), C5 uneven widths.
     Reported beside the headline line; not part of `value`."""
     import torch
     from paper_2210_09147_b200 import engine, model as mdl, streams
@@ -225,6 +225,8 @@ def extra_configs(peak):
               "sgd", "mse"),
              ("C4_adam_ce", "C4 with Adam and softmax-CE (PAPER.md:863 replay batches use Adam), D=8 on 1 GPU",
               [4096] * 33, 8, True, 16, 8, "adam", "softmax_ce"),
+             ("C4_m32", "C4's network with micro-batch 32 (replay window 32, SPEC.md:463), D=8 on 1 GPU",
+              [4096] * 33, 8, True, 32, 8, "sgd", "mse"),
              ("C5", "uneven widths 1024..8192 (24 layers), D=8 stages on 1 GPU", c5, 8, True, 1, 16, "sgd", "mse")]
     res = {}
     for name, desc, widths, D, learn, M, ticks, opt, loss in cases:

@@ -228,7 +228,7 @@ struct pt_pipeline {
   size_t rowbuf_floats = 0;
   int pn_nslot = 0, pn_va = 0, pn_vb = 0, pn_sown = 0, pn_sah = 0, pn_red = 0, pn_bar = 0, pn_desc = 0, pn_bias = 0,
       pn_smem = 0, pn_pf = 8;
-  // micro-batch tensor-core path (pt_tile.cuh): M == 16, widths % 256 == 0, single process
+  // micro-batch tensor-core path (pt_tile.cuh): M = 16, 32 or 64, widths % 256 == 0
   bool tile = false;
   int t_smem = 0, t_maxn = 0;
   float* t_part = nullptr;
@@ -576,6 +576,14 @@ int upload_tile_stages(pt_pipeline* p) {
   return PT_OK;
 }
 
+// The tile kernel instantiation of a handle: optimizer x micro-batch (16, 32 or 64).
+const void* tile_fn(const pt_pipeline* p) {
+  const bool adam = p->opt == PT_OPT_ADAM;
+  if (p->M == 64) return adam ? (const void*)pt::tile_kernel<1, 64> : (const void*)pt::tile_kernel<0, 64>;
+  if (p->M == 32) return adam ? (const void*)pt::tile_kernel<1, 32> : (const void*)pt::tile_kernel<0, 32>;
+  return adam ? (const void*)pt::tile_kernel<1, 16> : (const void*)pt::tile_kernel<0, 16>;
+}
+
 // Buffers, tensor maps and descriptors of the micro-batch tile path (pt_tile.cuh).
 int setup_tile(pt_pipeline* p) {
   const int M = p->M;
@@ -636,12 +644,10 @@ int setup_tile(pt_pipeline* p) {
   p->legacy_dirty = true;
   p->t_layers_host = tl;
   PT_TRY(upload_tile_stages(p));
-  // shared memory: 1 KB alignment slack, ring, lo, operands, delta tile, reductions, barriers
-  p->t_smem = 1024 + pt::T_NSLOT * pt::T_SLOT_FLOATS * 4 + pt::T_NB * 2 * M * pt::T_CK * 4 + pt::T_NB * 2 * pt::T_CK * pt::T_MAXM * 4 + 2 * 128 * pt::T_MAXM * 4 + 64 +
-              (3 * pt::T_NSLOT + 5 * pt::T_NB + 4) * 8 + 16;
+  // shared memory: 1 KB alignment slack, ring, operands, update operands, reductions, barriers
+  p->t_smem = M == 16 ? pt::TCfg<16>::smem_bytes() : M == 32 ? pt::TCfg<32>::smem_bytes() : pt::TCfg<64>::smem_bytes();
   if (p->t_smem > pt::SMEM_MAX) return fail(PT_EINVAL, "tile path shared-memory plan exceeds 227 KB");
-  CUDA_TRY(cudaFuncSetAttribute(pt::tile_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, p->t_smem));
-  CUDA_TRY(cudaFuncSetAttribute(pt::tile_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, p->t_smem));
+  CUDA_TRY(cudaFuncSetAttribute(tile_fn(p), cudaFuncAttributeMaxDynamicSharedMemorySize, p->t_smem));
   return PT_OK;
 }
 
@@ -885,9 +891,11 @@ int create_impl(const pt_config* c, pt_pipeline* p) {
     // stage kernel waiting for a neighbour (another handle, part or process) that is itself
     // blocked in such a load would only end at the watchdog.
     const void* others[] = {(const void*)pt::panel_kernel<0>, (const void*)pt::panel_kernel<1>,
-                            (const void*)pt::tile_kernel<0>, (const void*)pt::tl_to_blocks,
+                            (const void*)pt::tile_kernel<0, 16>, (const void*)pt::tl_to_blocks,
                             (const void*)pt::tl_from_blocks,
-                            (const void*)pt::tile_kernel<1>,
+                            (const void*)pt::tile_kernel<1, 16>, (const void*)pt::tile_kernel<0, 32>,
+                            (const void*)pt::tile_kernel<1, 32>, (const void*)pt::tile_kernel<0, 64>,
+                            (const void*)pt::tile_kernel<1, 64>,
                             (const void*)pt::epilogue_kernel, (const void*)pt::pn_to_tiles,
                             (const void*)pt::pn_from_tiles};
     cudaFuncAttributes fa;
@@ -900,8 +908,8 @@ int create_impl(const pt_config* c, pt_pipeline* p) {
   p->G = c->grid > 0 ? c->grid : sms;
   if (p->G > sms * per_sm) return fail(PT_EINVAL, "grid exceeds co-resident CTA capacity");
   {
-    // micro-batch tensor-core path: every width a multiple of 256, M == 16, all stages here
-    bool ok = p->M == 16;  // SGD or Adam, MSE or softmax-CE
+    // micro-batch tensor-core path: every width a multiple of 256, M = 16, 32 or 64
+    bool ok = p->M == 16 || p->M == 32 || p->M == 64;  // SGD or Adam, MSE or softmax-CE
     int units = 0;
     for (int i = 0; i <= p->L && ok; ++i) ok = (p->dims[i] % 256) == 0;
     for (int i = 0; i < p->L && ok; ++i) units = std::max(units, std::max(p->dims[i + 1], p->dims[i]) / 128 * pt::T_Q);
@@ -1705,7 +1713,7 @@ int run_impl(pt_pipeline* p, const float* xs, const float* ys, int64_t n, float*
     CUDA_TRY(cudaMemsetAsync(p->t_bars, 0, 32 * sizeof(u64), p->stream));
     void* targs[] = {&T};
     CUDA_TRY(cudaEventRecord(p->ev0, p->stream));
-    CUDA_TRY(cudaLaunchCooperativeKernel(p->opt == PT_OPT_ADAM ? (const void*)pt::tile_kernel<1> : (const void*)pt::tile_kernel<0>, dim3(p->G), dim3(pt::T_THREADS), targs,
+    CUDA_TRY(cudaLaunchCooperativeKernel(tile_fn(p), dim3(p->G), dim3(pt::T_THREADS), targs,
                                          size_t(p->t_smem), p->stream));
     CUDA_TRY(cudaEventRecord(p->ev1, p->stream));
   } else {

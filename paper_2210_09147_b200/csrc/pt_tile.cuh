@@ -35,18 +35,35 @@ namespace pt {
 constexpr int T_THREADS = 320;
 constexpr int T_SIMT0 = 64;            // first SIMT thread
 constexpr int T_NS = 256;              // SIMT threads
-constexpr int T_NSLOT = 5;             // weight ring slots of 32 KB
-constexpr int T_NB = 3;                // operand / lo-tile buffers (chunks in flight between SIMT and MMA)
 constexpr int T_SLOT_FLOATS = 8192;
 constexpr int T_CK = 64;               // F: chunk columns; B: chunk rows
 constexpr int T_Q = 4;                 // quarters (columns in F, rows in B)
-constexpr int T_MAXM = 16;
 constexpr int T_NACC = 1;              // independent accumulators per unit (K-step % T_NACC)
-constexpr int T_ACC_COLS = 2 * T_NACC * 32;  // TMEM columns of the two unit accumulators
-constexpr int T_TMEM_COLS = 512;        // accumulators, two 64-column lo tiles, two 128-column update tiles
-constexpr int T_LO_COL = T_ACC_COLS;    // lo tiles (A operand of the lo MMAs)
-constexpr int T_UPD_COL = T_ACC_COLS + T_NB * T_CK;  // update products D[c][r] (B steps)
-static_assert(T_UPD_COL + 2 * 128 <= T_TMEM_COLS, "TMEM plan exceeds the allocation");
+constexpr int T_TMEM_COLS = 512;
+// Per micro-batch size TM (16, 32 or 64; the batch is the MMA's N side, so a larger TM issues
+// the same F/B MMAs with a larger N): ring slots, operand / lo-tile buffers in flight (NB),
+// update-product buffers (NUB), and the TMEM plan = two unit accumulators of 2 TM columns,
+// NB 64-column lo tiles, NUB 128-column update products.
+template <int TM>
+struct TCfg {
+  static constexpr int NSLOT = TM == 16 ? 5 : TM == 32 ? 4 : 3;  // weight ring slots of 32 KB
+  static constexpr int NB = TM == 16 ? 3 : TM == 32 ? 2 : 1;     // chunks in flight between SIMT and MMA
+  static constexpr int NUB = TM == 64 ? 1 : 2;
+  static constexpr int ACC_COLS = 2 * T_NACC * 2 * TM;
+  static constexpr int LO_COL = ACC_COLS;
+  static constexpr int UPD_COL = ACC_COLS + NB * T_CK;
+  // dynamic shared memory: alignment slack, ring, operands (hi, lo), update operands,
+  // reduction scratch (TM floats), mbarriers, TMEM address
+  static constexpr int smem_bytes() {
+    return 1024 + NSLOT * T_SLOT_FLOATS * 4 + NB * 2 * TM * T_CK * 4 + NB * 2 * T_CK * TM * 4 + 2 * 128 * TM * 4 +
+           TM * 4 + (3 * NSLOT + 5 * NB + 4) * 8 + 16;
+  }
+};
+template <int TM>
+constexpr bool tcfg_fits() {
+  return TCfg<TM>::UPD_COL + TCfg<TM>::NUB * 128 <= T_TMEM_COLS && TCfg<TM>::smem_bytes() <= 227 * 1024;
+}
+static_assert(tcfg_fits<16>() && tcfg_fits<32>() && tcfg_fits<64>(), "tile kernel TMEM / shared-memory plan");
 constexpr int T_DTS = 24;              // dT row stride (floats): conflict-free staging, 16-B rows
 
 struct TLayer {
@@ -143,7 +160,7 @@ __device__ __forceinline__ void t_trace(const TParams& P, int& idx, int code) {
 
 // ------------------------------------------------------------------ schedule
 // The producer, the MMA issuer and the SIMT warps walk the same sequence of
-// (tick, stage, step, unit, chunk); chunk j uses ring slot j % T_NSLOT and operand /
+// (tick, stage, step, unit, chunk); chunk j uses ring slot j % C::NSLOT and operand /
 // lo buffer j % 2.
 struct TStep {
   int L;        // layer index
@@ -228,17 +245,17 @@ __device__ void t_grid_sync(const TParams& P, u64& gen) {
 }
 
 struct TSmem {
-  float* ring;      // T_NSLOT x 32 KB (1024-B aligned)
+  float* ring;      // C::NSLOT x 32 KB (1024-B aligned)
   float* opnd;      // 2 x (hi, lo) x [M][64] no-swizzle K-major
   float* dop;       // B: update MMA B operand [delta_hi; delta_lo]^T per chunk, [2][128][16]
   float* aop;       // B: update MMA A operand a^T (hi, lo) of the unit's 128 columns, [2][128][16]
-  float* red;       // 16 floats
-  uint64_t* full;   // [T_NSLOT]
-  uint64_t* sfree;  // [T_NSLOT] forward chunk in the slot consumed (MMA commit)
-  uint64_t* bfree;  // [T_NSLOT] backward chunk in the slot updated in place (4 write-back warps)
+  float* red;       // TM floats
+  uint64_t* full;   // [C::NSLOT]
+  uint64_t* sfree;  // [C::NSLOT] forward chunk in the slot consumed (MMA commit)
+  uint64_t* bfree;  // [C::NSLOT] backward chunk in the slot updated in place (4 write-back warps)
   uint64_t* opnd_rdy; // [2] operand chunk staged
-  uint64_t* prep;   // [T_NB] lo tile written (group A; the whole tile in B, K half 0 in F)
-  uint64_t* prep2;  // [T_NB] forward chunks: K half 1 of the lo tile written (group B)
+  uint64_t* prep;   // [C::NB] lo tile written (group A; the whole tile in B, K half 0 in F)
+  uint64_t* prep2;  // [C::NB] forward chunks: K half 1 of the lo tile written (group B)
   uint64_t* mhi;    // [2] hi MMAs of the chunk done (raw tile no longer read)
   uint64_t* mdone;  // [2] all MMAs of the chunk done
   uint64_t* afree;  // [2] accumulator read by the epilogue
@@ -247,7 +264,9 @@ struct TSmem {
 };
 
 // ------------------------------------------------------------------ producer
+template <int TM>
 __device__ void t_producer(const TParams& P, const TSmem& sm) {
+  using C = TCfg<TM>;
   const int c = blockIdx.x, G = P.G;
   uint32_t j = 0;
   for (int s = 0; s < P.n_stages; ++s)
@@ -258,11 +277,11 @@ __device__ void t_producer(const TParams& P, const TSmem& sm) {
   // per slot: kind of the chunk it holds (1 forward: released by the MMA commit on sfree,
   // 2 backward: released by the 4 write-back warps on bfree), completions consumed, and a
   // pending write-back (layer, row, col) of an updated backward tile
-  int kind[T_NSLOT];
-  uint32_t fcnt[T_NSLOT], bcnt[T_NSLOT];
-  int pend_l[T_NSLOT], pend_r[T_NSLOT], pend_c[T_NSLOT];
-  bool pend[T_NSLOT];
-  for (int s = 0; s < T_NSLOT; ++s) {
+  int kind[C::NSLOT];
+  uint32_t fcnt[C::NSLOT], bcnt[C::NSLOT];
+  int pend_l[C::NSLOT], pend_r[C::NSLOT], pend_c[C::NSLOT];
+  bool pend[C::NSLOT];
+  for (int s = 0; s < C::NSLOT; ++s) {
     pend[s] = false;
     kind[s] = 0;
     fcnt[s] = bcnt[s] = 0;
@@ -307,7 +326,7 @@ __device__ void t_producer(const TParams& P, const TSmem& sm) {
         for (int u = c; u < sp.nunits; u += G) {
           const int blk = u / T_Q, q = u % T_Q;
           for (int ch = 0; ch < sp.nchunks; ++ch, ++j) {
-            const int slot = j % T_NSLOT;
+            const int slot = j % C::NSLOT;
             if (pend[slot]) {
               flush(slot);
               bulk_commit();
@@ -344,7 +363,7 @@ __device__ void t_producer(const TParams& P, const TSmem& sm) {
     }
     if (P.learn) {
       // end of tick: write back every updated tile still in the ring, then publish
-      for (uint32_t k = 0; k < T_NSLOT; ++k) flush(int((j + k) % T_NSLOT));
+      for (uint32_t k = 0; k < C::NSLOT; ++k) flush(int((j + k) % C::NSLOT));
       bulk_commit();
       bulk_wait_all();
       fence_proxy_async_global();
@@ -354,7 +373,9 @@ __device__ void t_producer(const TParams& P, const TSmem& sm) {
 }
 
 // ------------------------------------------------------------------ MMA issuer
+template <int TM>
 __device__ void t_mma(const TParams& P, const TSmem& sm, uint32_t tbase) {
+  using C = TCfg<TM>;
   // Per K-step two MMAs: hi(W) x [a_hi; a_lo] (N = 2M) and lo(W) x a_hi (N = M), both into
   // the unit accumulator: columns [0, M) collect hi*a_hi + lo*a_hi, [M, 2M) hi*a_lo.
   // The hi MMAs read the raw TMA tile (the tensor core uses its top 19 bits = tf32(w)),
@@ -375,14 +396,14 @@ __device__ void t_mma(const TParams& P, const TSmem& sm, uint32_t tbase) {
           const uint32_t acc = tbase + (uc & 1) * uint32_t(T_NACC * 2 * M);
           if (uc >= 2) t_wait(&sm.afree[uc & 1], ((uc - 2) >> 1) & 1, P);
           for (int ch = 0; ch < sp.nchunks; ++ch, ++j) {
-            const int slot = j % T_NSLOT, b = j % T_NB;
+            const int slot = j % C::NSLOT, b = j % C::NB;
             const float* hi = sm.ring + size_t(slot) * T_SLOT_FLOATS;
             const float* opn = sm.opnd + size_t(b) * 2 * M * T_CK;
-            t_wait(&sm.opnd_rdy[b], (j / T_NB) & 1, P);  // operands (group B)
-            t_wait(&sm.full[slot], (j / T_NSLOT) & 1, P);
-            t_wait(&sm.prep[b], (j / T_NB) & 1, P);  // lo tile in TMEM (group A)
+            t_wait(&sm.opnd_rdy[b], (j / C::NB) & 1, P);  // operands (group B)
+            t_wait(&sm.full[slot], (j / C::NSLOT) & 1, P);
+            t_wait(&sm.prep[b], (j / C::NB) & 1, P);  // lo tile in TMEM (group A)
             if (sp.fwd) {
-              t_wait(&sm.prep2[fj % T_NB], (fj / T_NB) & 1, P);  // its second K half (group B)
+              t_wait(&sm.prep2[fj % C::NB], (fj / C::NB) & 1, P);  // its second K half (group B)
               ++fj;
             }
             t_trace(P, tr, 20);
@@ -392,7 +413,7 @@ __device__ void t_mma(const TParams& P, const TSmem& sm, uint32_t tbase) {
             // MN-major SW128_32B: +8 rows = 1 KB; operand (no swizzle): +256 B
             const uint64_t da = sp.fwd ? tc_desc_kmajor_sw128(hi, 0) : tc_desc_mn_sw128b32(hi, 0, 8192);
             const uint64_t db = tc_desc_kmajor_noswz(opn, 0, T_CK);
-            const uint32_t lot = tbase + T_LO_COL + uint32_t(b) * T_CK;  // lo tile in TMEM
+            const uint32_t lot = tbase + C::LO_COL + uint32_t(b) * T_CK;  // lo tile in TMEM
 #pragma unroll
             for (int ks = 0; ks < T_CK / 8; ++ks) {
               const uint64_t dak = sp.fwd ? da + uint64_t((ks >> 2) * 1024 + (ks & 3) * 2) : da + uint64_t(ks * 64);
@@ -400,22 +421,22 @@ __device__ void t_mma(const TParams& P, const TSmem& sm, uint32_t tbase) {
               tc_mma_tf32_ts(acc, lot + ks * 8, db + uint64_t(ks * 16), id1, true);
             }
             if (!sp.fwd) {
-              // the update product goes to TMEM buffer bj % 2, free once group B applied bj - 2
-              const uint32_t ubuf = bj & 1;
-              if (bj >= 2) t_wait(&sm.applied[ubuf], ((bj - 2) >> 1) & 1, P);
+              // the update product goes to TMEM buffer bj % NUB, free once group B applied bj - NUB
+              const uint32_t ubuf = bj % C::NUB;
+              if (bj >= C::NUB) t_wait(&sm.applied[ubuf], ((bj - C::NUB) / C::NUB) & 1, P);
               tc_fence_after();
               if (upd) {
                 // D[c][r] = sum_m a[m][c] delta[m][r] over K = m (2 K-steps):
                 // a_hi x [delta_hi; delta_lo] (N = 128) and a_lo x delta_hi (N = 64)
-                const uint64_t ua = tc_desc_kmajor_noswz(sm.aop, 0, T_MAXM);
-                const uint64_t ual = tc_desc_kmajor_noswz(sm.aop + 128 * T_MAXM, 0, T_MAXM);
-                const uint64_t ub = tc_desc_kmajor_noswz(sm.dop + size_t(b) * 2 * T_CK * T_MAXM, 0, T_MAXM);
-                const uint32_t ud = tbase + T_UPD_COL + ubuf * 128;
+                const uint64_t ua = tc_desc_kmajor_noswz(sm.aop, 0, TM);
+                const uint64_t ual = tc_desc_kmajor_noswz(sm.aop + 128 * TM, 0, TM);
+                const uint64_t ub = tc_desc_kmajor_noswz(sm.dop + size_t(b) * 2 * T_CK * TM, 0, TM);
+                const uint32_t ud = tbase + C::UPD_COL + ubuf * 128;
 #pragma unroll
-                for (int kk = 0; kk < T_MAXM / 8; ++kk)
+                for (int kk = 0; kk < TM / 8; ++kk)
                   tc_mma_tf32(ud, ua + uint64_t(kk * 16), ub + uint64_t(kk * 16), idu2, kk > 0);
 #pragma unroll
-                for (int kk = 0; kk < T_MAXM / 8; ++kk)
+                for (int kk = 0; kk < TM / 8; ++kk)
                   tc_mma_tf32(ud, ual + uint64_t(kk * 16), ub + uint64_t(kk * 16), idu1, true);
               }
               ++bj;
@@ -435,35 +456,37 @@ __device__ void t_mma(const TParams& P, const TSmem& sm, uint32_t tbase) {
 // no-swizzle K-major layout. Two phases so the L2 loads of chunk j+1 are in flight while
 // chunk j is processed: fetch() issues the loads into registers, put() stores them.
 // With dT != nullptr (B chunks), the exact values are also kept as dT[k][m] for the update.
+template <int TM>
 struct TOpnd {
-  // group A thread -> 8 elements (m, k): lane = (m % 8) * 4 + k % 4, so every warp store of
-  // the no-swizzle core-matrix layout hits 32 distinct banks (M == 16: 2 row groups x 16
-  // k-quads)
-  float v[8];
+  // group B thread -> TM / 2 elements (m, k): lane = (m % 8) * 4 + k % 4, so every warp store
+  // of the no-swizzle core-matrix layout hits 32 distinct banks (TM / 8 row groups x 16
+  // k-quads, split over the 4 warps)
+  static constexpr int NQ = TM / 2, MG = TM / 8;
+  float v[NQ];
   __device__ __forceinline__ void fetch(const float* src, int ld, int) {
     const int st = (threadIdx.x - T_SIMT0) & (T_GRP - 1), lane = st & 31, w = st >> 5;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int idx = w * 8 + q, m = (idx & 1) * 8 + (lane >> 2), k = (idx >> 1) * 4 + (lane & 3);
+    for (int q = 0; q < NQ; ++q) {
+      const int idx = w * NQ + q, m = (idx % MG) * 8 + (lane >> 2), k = (idx / MG) * 4 + (lane & 3);
       v[q] = __ldcg(src + size_t(m) * ld + k);
     }
   }
   // dop != nullptr (B chunks): also the update MMA's B operand [delta_hi; delta_lo]^T, rows
-  // r (64 hi + 64 lo) x K = m (16), no-swizzle K-major (SBO 512 B)
+  // r (64 hi + 64 lo) x K = m (TM), no-swizzle K-major
   __device__ __forceinline__ void put(float* ohi, float* olo, float* dop, int) const {
     const int st = (threadIdx.x - T_SIMT0) & (T_GRP - 1), lane = st & 31, w = st >> 5;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int idx = w * 8 + q, mg = idx & 1, kq = idx >> 1;
+    for (int q = 0; q < NQ; ++q) {
+      const int idx = w * NQ + q, mg = idx % MG, kq = idx / MG;
       const int off = mg * 512 + kq * 32 + lane;  // == tc_kmajor_noswz_off(m, k, 64) / 4
       const float h = tf32_hi(v[q]);
       ohi[off] = h;
       olo[off] = v[q] - h;
       if (dop) {
         const int r = kq * 4 + (lane & 3), m = mg * 8 + (lane >> 2);
-        const int o2 = int(tc_kmajor_noswz_off(r, m, T_MAXM) >> 2);
+        const int o2 = int(tc_kmajor_noswz_off(r, m, TM) >> 2);
         dop[o2] = h;
-        dop[o2 + T_CK * T_MAXM] = v[q] - h;
+        dop[o2 + T_CK * TM] = v[q] - h;
       }
     }
   }
@@ -650,8 +673,9 @@ __global__ void tl_from_blocks(const float* __restrict__ src, float* __restrict_
 
 // OPT: 0 SGD, 1 Adam (separate instantiations: the Adam moments' registers stay out of the
 // SGD kernel)
-template <int OPT>
+template <int OPT, int TM>
 __global__ void __launch_bounds__(T_THREADS, 1) tile_kernel(const __grid_constant__ TParams P) {
+  using C = TCfg<TM>;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1024-B alignment of the swizzled tiles
   // (pointer arithmetic on smem_raw, not integer casts, so the compiler keeps the shared
@@ -661,31 +685,31 @@ __global__ void __launch_bounds__(T_THREADS, 1) tile_kernel(const __grid_constan
   const int M = P.M, G = P.G, c = blockIdx.x;
   const int ob = M * T_CK;
   sm.ring = reinterpret_cast<float*>(base);
-  sm.opnd = sm.ring + T_NSLOT * T_SLOT_FLOATS;
-  sm.dop = sm.opnd + T_NB * 2 * ob;
-  sm.aop = sm.dop + T_NB * 2 * T_CK * T_MAXM;
-  sm.red = sm.aop + 2 * 128 * T_MAXM;
-  sm.full = reinterpret_cast<uint64_t*>(sm.red + 16);
-  sm.sfree = sm.full + T_NSLOT;
-  sm.bfree = sm.sfree + T_NSLOT;
-  sm.opnd_rdy = sm.bfree + T_NSLOT;
-  sm.prep = sm.opnd_rdy + T_NB;
-  sm.prep2 = sm.prep + T_NB;
-  sm.mhi = sm.prep2 + T_NB;
-  sm.mdone = sm.mhi + T_NB;
-  sm.afree = sm.mdone + T_NB;
+  sm.opnd = sm.ring + C::NSLOT * T_SLOT_FLOATS;
+  sm.dop = sm.opnd + C::NB * 2 * ob;
+  sm.aop = sm.dop + C::NB * 2 * T_CK * TM;
+  sm.red = sm.aop + 2 * 128 * TM;
+  sm.full = reinterpret_cast<uint64_t*>(sm.red + TM);
+  sm.sfree = sm.full + C::NSLOT;
+  sm.bfree = sm.sfree + C::NSLOT;
+  sm.opnd_rdy = sm.bfree + C::NSLOT;
+  sm.prep = sm.opnd_rdy + C::NB;
+  sm.prep2 = sm.prep + C::NB;
+  sm.mhi = sm.prep2 + C::NB;
+  sm.mdone = sm.mhi + C::NB;
+  sm.afree = sm.mdone + C::NB;
   sm.applied = sm.afree + 2;
   sm.tmem = reinterpret_cast<uint32_t*>(sm.applied + 2);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     // barriers arrived by a SIMT group count its 4 warps (one arrival per warp, no group
     // barrier needed); tensor-core commits and the producer arrive once
-    for (int s = 0; s < T_NSLOT; ++s) {
+    for (int s = 0; s < C::NSLOT; ++s) {
       mbar_init(&sm.full[s], 1);
       mbar_init(&sm.sfree[s], 1);
       mbar_init(&sm.bfree[s], 4);
     }
-    for (int b = 0; b < T_NB; ++b) {
+    for (int b = 0; b < C::NB; ++b) {
       mbar_init(&sm.opnd_rdy[b], 4);
       mbar_init(&sm.mhi[b], 1);
       mbar_init(&sm.prep[b], 4);
@@ -705,9 +729,9 @@ __global__ void __launch_bounds__(T_THREADS, 1) tile_kernel(const __grid_constan
   const uint32_t tbase = *sm.tmem;
 
   if (warp == 0) {
-    if (lane == 0) t_producer(P, sm);
+    if (lane == 0) t_producer<TM>(P, sm);
   } else if (warp == 1) {
-    if (lane == 0) t_mma(P, sm, tbase);
+    if (lane == 0) t_mma<TM>(P, sm, tbase);
   } else {
     // ================================================================ SIMT
     const int st_id = tid - T_SIMT0;           // 0..255
@@ -763,12 +787,12 @@ __global__ void __launch_bounds__(T_THREADS, 1) tile_kernel(const __grid_constan
           if (!sp.fwd && upd) {
             // bias of this layer, rows spread over the grid: b -= lr * sum_m delta
             for (int r = gtid; r < L.n_out; r += gthreads) {
-              float dv[T_MAXM];
+              float dv[TM];
 #pragma unroll
-              for (int m = 0; m < T_MAXM; ++m) dv[m] = m < M ? t_ld(P.delta + size_t(m) * P.max_n + r) : 0.f;
+              for (int m = 0; m < TM; ++m) dv[m] = m < M ? t_ld(P.delta + size_t(m) * P.max_n + r) : 0.f;
               float sd = 0.f;
 #pragma unroll
-              for (int m = 0; m < T_MAXM; ++m) sd += dv[m];
+              for (int m = 0; m < TM; ++m) sd += dv[m];
               if (OPT == 1) {
                 float mm = t_ld(L.mb + r), vv = t_ld(L.vb + r);
                 L.b[r] = t_adam1(t_ld(L.b + r), sd, mm, vv, P, c1, c2);
@@ -786,13 +810,13 @@ __global__ void __launch_bounds__(T_THREADS, 1) tile_kernel(const __grid_constan
             if (grp == 0) {
               // ===================== group A: lo tiles (TMEM), accumulator epilogue
               for (int ch = 0; ch < sp.nchunks; ++ch, ++j) {
-                const int slot = j % T_NSLOT, b = j % T_NB;
+                const int slot = j % C::NSLOT, b = j % C::NB;
                 const float* tile = sm.ring + size_t(slot) * T_SLOT_FLOATS;
-                const uint32_t lot = tbase + T_LO_COL + uint32_t(b) * T_CK;  // lo tile in TMEM
+                const uint32_t lot = tbase + C::LO_COL + uint32_t(b) * T_CK;  // lo tile in TMEM
                 t_trace(P, tr, 6);
-                if (j >= T_NB) t_wait(&sm.mdone[b], ((j - T_NB) / T_NB) & 1, P);  // lo buffer free
+                if (j >= C::NB) t_wait(&sm.mdone[b], ((j - C::NB) / C::NB) & 1, P);  // lo buffer free
                 tc_fence_after();
-                t_wait(&sm.full[slot], (j / T_NSLOT) & 1, P);
+                t_wait(&sm.full[slot], (j / C::NSLOT) & 1, P);
                 t_trace(P, tr, 7);
                 if (sp.fwd) t_lo_pass_f(tile, lot, 0, 1);
                 else t_lo_pass_b(tile, lot);
@@ -803,19 +827,27 @@ __global__ void __launch_bounds__(T_THREADS, 1) tile_kernel(const __grid_constan
               }
               // unit epilogue: last chunk's MMAs complete -> accumulator -> quarter partials
               const uint32_t jl = j - 1;
-              t_wait(&sm.mdone[jl % T_NB], (jl / T_NB) & 1, P);
+              t_wait(&sm.mdone[jl % C::NB], (jl / C::NB) & 1, P);
               tc_fence_after();
               {
                 const int lq = warp & 3;
                 const uint32_t ta = tbase + (uc & 1) * uint32_t(T_NACC * 2 * M) + ((uint32_t(lq) * 32) << 16);
-                float v[16], vv[32];
-                tmem_ld_32x32b_x32(ta, vv);  // one load + wait: columns [0,16) and [16,32)
-#pragma unroll
-                for (int m = 0; m < 16; ++m) v[m] = vv[m] + vv[16 + m];  // (hi + lo) * a_hi + hi * a_lo
                 const int rowcol = blk * 128 + lq * 32 + lane;  // F: output row; B: input column
                 float* dst = P.part + size_t(q) * M * P.max_n + rowcol;
+                if constexpr (TM == 16) {
+                  float vv[32];
+                  tmem_ld_32x32b_x32(ta, vv);  // one load + wait: columns [0,16) and [16,32)
 #pragma unroll
-                for (int m = 0; m < 16; ++m) dst[size_t(m) * P.max_n] = v[m];
+                  for (int m = 0; m < 16; ++m) dst[size_t(m) * P.max_n] = vv[m] + vv[16 + m];  // (hi + lo) * a_hi + hi * a_lo
+                } else {
+#pragma unroll
+                  for (int hh = 0; hh < TM / 32; ++hh) {
+                    float v0[32], v1[32];
+                    tmem_ld_2x32(ta + 32 * hh, ta + TM + 32 * hh, v0, v1);  // columns of samples 32 hh.. in [0, TM) and [TM, 2 TM)
+#pragma unroll
+                    for (int m = 0; m < 32; ++m) dst[size_t(32 * hh + m) * P.max_n] = v0[m] + v1[m];
+                  }
+                }
               }
               tc_fence_before();
               __syncwarp();
@@ -828,13 +860,13 @@ __global__ void __launch_bounds__(T_THREADS, 1) tile_kernel(const __grid_constan
                 // cache), tf32 hi / lo, no-swizzle K-major [128][16]; published with chunk
                 // 0's operands. The previous unit's MMAs are complete (its last apply waited).
                 const int cbase = blk * 128;
-                for (int e = gst; e < 128 * T_MAXM; e += T_GRP) {
+                for (int e = gst; e < 128 * TM; e += T_GRP) {
                   const int m = e >> 7, cc = e & 127;
                   const float x = t_ld(Cb + L.a_in + size_t(m) * L.n_in + cbase + cc);
-                  const int o = int(tc_kmajor_noswz_off(cc, m, T_MAXM) >> 2);
+                  const int o = int(tc_kmajor_noswz_off(cc, m, TM) >> 2);
                   const float h = tf32_hi(x);
                   sm.aop[o] = h;
-                  sm.aop[128 * T_MAXM + o] = x - h;
+                  sm.aop[128 * TM + o] = x - h;
                 }
               }
               // operand source of chunk ch: F = a_i[:, cols], B = delta[:, rows]
@@ -848,18 +880,18 @@ __global__ void __launch_bounds__(T_THREADS, 1) tile_kernel(const __grid_constan
                 osrc = P.delta + q * (L.n_out / T_Q);
                 old = P.max_n;
               }
-              TOpnd op;
+              TOpnd<TM> op;
               op.fetch(osrc, old, M);
               auto apply = [&](uint32_t jj, uint32_t bb, int chn) {
                 // chunk jj: all its MMAs are done -> SGD step in place -> producer stores the tile
-                const int pslot = jj % T_NSLOT;
-                t_wait(&sm.mdone[jj % T_NB], (jj / T_NB) & 1, P);
+                const int pslot = jj % C::NSLOT;
+                t_wait(&sm.mdone[jj % C::NB], (jj / C::NB) & 1, P);
                 tc_fence_after();
                 t_trace(P, tr, 9);
                 if (upd) {
                   // Adam: this chunk's rows r0.. and the unit's 128 columns c0.. of the moments
                   const size_t mo = size_t(q * (L.n_out / T_Q) + chn * T_CK) * L.ld + size_t(blk) * 128;
-                  t_apply_update<OPT == 1>(sm.ring + size_t(pslot) * T_SLOT_FLOATS, tbase + T_UPD_COL + (bb & 1) * 128, nlr, P,
+                  t_apply_update<OPT == 1>(sm.ring + size_t(pslot) * T_SLOT_FLOATS, tbase + C::UPD_COL + (bb % C::NUB) * 128, nlr, P,
                                  OPT == 1 ? L.mW + mo : nullptr, OPT == 1 ? L.vW + mo : nullptr, L.ld, c1, c2);
                   fence_proxy_async_shared();  // W' -> the producer's TMA store
                 }
@@ -867,31 +899,31 @@ __global__ void __launch_bounds__(T_THREADS, 1) tile_kernel(const __grid_constan
                 __syncwarp();
                 if (lane == 0) {
                   mbar_arrive(&sm.bfree[pslot]);
-                  mbar_arrive(&sm.applied[bb & 1]);
+                  mbar_arrive(&sm.applied[bb % C::NUB]);
                 }
                 t_trace(P, tr, 10);
               };
               for (int ch = 0; ch < sp.nchunks; ++ch, ++j) {
-                const int b = j % T_NB;
+                const int b = j % C::NB;
                 float* ohi = sm.opnd + size_t(b) * 2 * ob;
-                float* dopb = sm.dop + size_t(b) * 2 * T_CK * T_MAXM;
+                float* dopb = sm.dop + size_t(b) * 2 * T_CK * TM;
                 t_trace(P, tr, 8);
-                if (j >= T_NB) t_wait(&sm.mdone[b], ((j - T_NB) / T_NB) & 1, P);  // operand buffers free
+                if (j >= C::NB) t_wait(&sm.mdone[b], ((j - C::NB) / C::NB) & 1, P);  // operand buffers free
                 tc_fence_after();
                 op.put(ohi, ohi + ob, sp.fwd ? nullptr : dopb, M);
                 if (ch + 1 < sp.nchunks) op.fetch(osrc + (ch + 1) * T_CK, old, M);
                 fence_proxy_async_shared();  // operands -> the tensor core (async proxy)
                 if (sp.fwd) {
                   // forward: group B also writes K half 1 of the lo tile
-                  const int slot = j % T_NSLOT;
-                  t_wait(&sm.full[slot], (j / T_NSLOT) & 1, P);
-                  t_lo_pass_f(sm.ring + size_t(slot) * T_SLOT_FLOATS, tbase + T_LO_COL + uint32_t(b) * T_CK, 1, 2);
+                  const int slot = j % C::NSLOT;
+                  t_wait(&sm.full[slot], (j / C::NSLOT) & 1, P);
+                  t_lo_pass_f(sm.ring + size_t(slot) * T_SLOT_FLOATS, tbase + C::LO_COL + uint32_t(b) * T_CK, 1, 2);
                   tc_fence_before();
                 }
                 __syncwarp();
                 if (lane == 0) {
                   mbar_arrive(&sm.opnd_rdy[b]);
-                  if (sp.fwd) mbar_arrive(&sm.prep2[fj % T_NB]);
+                  if (sp.fwd) mbar_arrive(&sm.prep2[fj % C::NB]);
                 }
                 if (sp.fwd) ++fj;
                 if (!sp.fwd) {

@@ -14,6 +14,8 @@ from paper_2210_09147_b200 import engine, model as mdl, streams  # noqa: E402
 CASES = {"tile": ([256, 512, 512, 256, 256], 16), "tick": ([32, 64, 64, 64, 16], 1),
          "panel": ([32, 64, 64, 64, 16], 1), "panel_wide": ([256, 512, 512, 512, 128], 1),
          "panel_adam": ([256, 512, 512, 512, 128], 1), "tile_adam": ([256, 512, 512, 256, 256], 16),
+         "tile_m32": ([256, 512, 512, 256, 256], 32), "tile_m32_adam": ([256, 512, 512, 256, 256], 32),
+         "tile_m64": ([256, 512, 512, 256, 256], 64), "tile_m64_adam": ([256, 512, 512, 256, 256], 64),
          "tick_mb": ([64, 96, 96, 96, 32], 4), "tick_conc": ([256] * 9, 1), "tick_conc_mb": ([128] * 9, 4),
          "tick_mb_wide": ([1218, 3805, 2590, 1500], 2)}
 

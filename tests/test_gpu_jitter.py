@@ -20,6 +20,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
                                                ("tick", "4,3", "1"), ("tick_mb", "4,3", "1"),
                                                ("panel", "4,3", "1"), ("panel", "7", "0"), ("panel_wide", "2,2,3", "1"),
                                                ("panel_adam", "4,3", "1"), ("tile_adam", "4,3", "1"),
+                                               ("tile_m32", "4,3", "1"), ("tile_m32_adam", "4,3", "1"),
+                                               ("tile_m64", "4,3", "1"), ("tile_m64_adam", "4,3", "1"),
                                                ("tick_conc", "8,7", "1"), ("tick_conc", "4,4,4,3", "1"),
                                                ("tick_conc_mb", "6,4,5", "1"), ("tick_mb_wide", "2,2,1", "1")])
 def test_jitter_bitwise(kind, counts, learn):

@@ -328,66 +328,77 @@ def test_paper_pipeline_api():
 
 
 # ---------------------------------------------------------------- tensor-core tile path
-# batch 16 with every width a multiple of 256 runs pt::tile_kernel (tcgen05, 3xTF32)
+# micro-batch 16, 32 or 64 with every width a multiple of 256 runs pt::tile_kernel (tcgen05,
+# 3xTF32; the batch is the MMA's N side, one instantiation per TM)
 
-def _tile_case(widths, counts, T, lr, **kw):
-    e = _case(widths, counts, T, lr, M=16, **kw)
+TILE_M = pytest.mark.parametrize("TM", [16, 32, 64])
+
+
+def _tile_case(widths, counts, T, lr, TM=16, **kw):
+    e = _case(widths, counts, T, lr, M=TM, **kw)
     return e
 
 
-def test_tile_path_selected():
-    m, st, mk = _pipe([256, 512, 256], [2, 1], 0.01, M=16)
+@TILE_M
+def test_tile_path_selected(TM):
+    m, st, mk = _pipe([256, 512, 256], [2, 1], 0.01, M=TM)
     xs, ys = st.block(0, 2)
     p = mk(xs, ys)
     assert p.kernel_path == "tile"
     p.close()
-    m, st, mk = _pipe([64, 256, 128, 32], [2, 3], 0.01, M=16)
+    m, st, mk = _pipe([64, 256, 128, 32], [2, 3], 0.01, M=TM)
     xs, ys = st.block(0, 2)
     p = mk(xs, ys)
     assert p.kernel_path == "tick"
     p.close()
 
 
+@TILE_M
 @pytest.mark.parametrize("D", [1, 2])
-def test_tile_small(D):
+def test_tile_small(D, TM):
     counts = {1: [5], 2: [2, 3]}[D]
-    _tile_case([256, 512, 256, 256], counts, 12, 0.02)
+    _tile_case([256, 512, 256, 256], counts, 12, 0.02, TM=TM)
 
 
+@TILE_M
 @pytest.mark.parametrize("opt,loss,D", [("adam", "mse", 1), ("sgd", "softmax_ce", 2), ("adam", "softmax_ce", 2)])
-def test_tile_adam_softmax_ce(opt, loss, D):
+def test_tile_adam_softmax_ce(opt, loss, D, TM):
     """Adam and softmax-CE on the tcgen05 tile kernel (PAPER.md:863 runs
     the replay-batch experiment with Adam)."""
     widths, counts = [256, 512, 256, 256], {1: [5], 2: [2, 3]}[D]
-    m, st, mk = _pipe(widths, counts, 0.01, M=16)
+    m, st, mk = _pipe(widths, counts, 0.01, M=TM)
     xs, ys = st.block(0, 2)
     p = engine.Pipeline(mdl.mlp(widths, seed=0, loss=loss), counts, opt, 1e-3,
-                        xs[0], ys[0] if loss == "mse" else np.zeros(16, np.float32))
+                        xs[0], ys[0] if loss == "mse" else np.zeros(TM, np.float32))
     assert p.kernel_path == "tile"
     p.close()
-    _tile_case(widths, counts, 12, 1e-3 if opt == "adam" else 0.02, optimizer=opt, loss=loss)
+    _tile_case(widths, counts, 12, 1e-3 if opt == "adam" else 0.02, optimizer=opt, loss=loss, TM=TM)
 
 
+@TILE_M
 @pytest.mark.parametrize("act_delay", [0, 1])
-def test_tile_act_delay_tanh(act_delay):
-    _tile_case([256, 256, 512, 256], [2, 3], 10, 0.02, act="tanh", act_delay=act_delay)
+def test_tile_act_delay_tanh(act_delay, TM):
+    _tile_case([256, 256, 512, 256], [2, 3], 10, 0.02, act="tanh", act_delay=act_delay, TM=TM)
 
 
-def test_tile_inference():
-    _tile_case([512, 1024, 512, 256], [2, 3], 6, 0.0, learn=False)
+@TILE_M
+def test_tile_inference(TM):
+    _tile_case([512, 1024, 512, 256], [2, 3], 6, 0.0, learn=False, TM=TM)
 
 
-def test_tile_c4_shape():
-    """Config 4 shapes (4096 wide, batch 16): 4 layers, D=1 and D=2, against the f64 oracle."""
-    _tile_case([4096] * 5, [7], 3, 1e-3)
-    _tile_case([4096] * 5, [4, 3], 4, 1e-3)
+@TILE_M
+def test_tile_c4_shape(TM):
+    """Config 4 shapes (4096 wide, micro-batch 16 / 32): 4 layers, D=1 and D=2, against the f64 oracle."""
+    _tile_case([4096] * 5, [7], 3, 1e-3, TM=TM)
+    _tile_case([4096] * 5, [4, 3], 4, 1e-3, TM=TM)
 
 
-def test_tile_deterministic_and_split():
+@TILE_M
+def test_tile_deterministic_and_split(TM):
     """Fixed reduction orders: identical runs are bitwise equal, also when split over calls."""
     res = []
     for split in (False, True):
-        m, st, mk = _pipe([256, 512, 512, 256], [2, 3], 0.02, M=16)
+        m, st, mk = _pipe([256, 512, 512, 256], [2, 3], 0.02, M=TM)
         xs, ys = st.block(0, 8)
         xs, ys = xs.astype(np.float32), ys.astype(np.float32)
         p = mk(xs, ys)
@@ -403,14 +414,16 @@ def test_tile_deterministic_and_split():
         assert np.array_equal(Wa, Wb) and np.array_equal(ba, bb)
 
 
-def test_tile_non_pow2_widths_d3():
+@TILE_M
+def test_tile_non_pow2_widths_d3(TM):
     """Widths 768 / 1280 (padded row pitch != width) and three stages on one GPU."""
-    _tile_case([256, 768, 1280, 512, 256], [2, 2, 3], 9, 0.02)
+    _tile_case([256, 768, 1280, 512, 256], [2, 2, 3], 9, 0.02, TM=TM)
 
 
-def test_tile_small_grid():
+@TILE_M
+def test_tile_small_grid(TM):
     """Fewer CTAs than work units: every CTA walks several units per step."""
-    _tile_case([512, 1024, 512, 256], [2, 3], 6, 0.02, grid=24)
+    _tile_case([512, 1024, 512, 256], [2, 3], 6, 0.02, grid=24, TM=TM)
 
 
 

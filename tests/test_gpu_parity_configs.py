@@ -6,7 +6,7 @@ shape, kernel and stage count:
 
 - C2: 32 x 2048 ReLU MLP, batch 1, learning, N = 50 ticks (SURVEY §8(c)) at D = 1, 2 and 8;
 - C3: 64 x 4096 inference wave, D = 8, 16 ticks;
-- C4: 32 x 4096, micro-batch 16 (tcgen05 tile kernel), D = 8, 8 ticks;
+- C4: 32 x 4096, micro-batch 16 and 32 (tcgen05 tile kernel), D = 8, 8 ticks;
 - C5: uneven widths 1024..8192 (24 layers), DP-balanced (bench.balanced_counts), D = 8, 8 ticks.
 
 The oracle runs on the host in f64 and f32 (numpy + BLAS); the C4/C5 cases take a minute or
@@ -46,16 +46,18 @@ def test_c3_inference_d8():
     _case(w, _bench_counts(w, 8, False), 16, 0.0, learn=False)
 
 
-def test_c4_tile_d8():
-    """Config 4: 32 x 4096, micro-batch 16 on the tcgen05 tile kernel, D = 8, 8 ticks."""
+@pytest.mark.parametrize("M", [16, 32])
+def test_c4_tile_d8(M):
+    """Config 4: 32 x 4096, micro-batch 16 (and 32, bench's C4_m32 line) on the tcgen05 tile
+    kernel, D = 8, 8 ticks."""
     from paper_2210_09147_b200 import engine, model as mdl
     w = [4096] * 33
     counts = _bench_counts(w, 8, True)
-    p = engine.Pipeline(mdl.mlp(w, seed=0), counts, "sgd", 1e-3, np.zeros((16, 4096), np.float32),
-                        np.zeros((16, 4096), np.float32))
+    p = engine.Pipeline(mdl.mlp(w, seed=0), counts, "sgd", 1e-3, np.zeros((M, 4096), np.float32),
+                        np.zeros((M, 4096), np.float32))
     assert p.kernel_path == "tile"
     p.close()
-    _case(w, counts, 8, 1e-3, M=16)
+    _case(w, counts, 8, 1e-3, M=M)
 
 
 def test_c4_tile_d8_adam_ce():
