@@ -242,6 +242,10 @@ def extra_configs(peak):
             y0 = ys[0].cpu().numpy() if M > 1 else ys[0, 0].cpu().numpy()
             p = engine.Pipeline(m, balanced_counts(widths, D, learn), opt, (1e-3 if opt == "sgd" else 1e-4)
                                 if learn else 0.0, x0, y0, learn=learn)
+            # untimed runs until every stage is past its warm-up gate (t >= 2D - h - 1):
+            # before it a stage neither updates nor writes its weights back
+            for _ in range(-(-(2 * D - 1) // ticks)):
+                p.run(xs, ys)
             best = 1e30
             for _ in range(3):
                 p.run(xs, ys)

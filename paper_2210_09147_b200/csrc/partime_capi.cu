@@ -594,18 +594,28 @@ int setup_tile(pt_pipeline* p) {
   PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&p->t_delta), size_t(M) * maxn * 4));
   PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&p->t_bars), 32 * sizeof(u64)));
   PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&p->t_ce), size_t(p->G) * M * 2 * 4));
-  std::vector<CUtensorMap> maps(2 * p->layers.size());
+  // per layer: W forward / backward boxes, and with Adam the L2-prefetch maps of m and v
+  std::vector<CUtensorMap> maps(4 * p->layers.size());
   std::vector<pt::TLayer> tl(p->layers.size());
   PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&p->d_tmaps), maps.size() * sizeof(CUtensorMap)));
   for (size_t i = 0; i < p->layers.size(); ++i) {
     const LayerHost& Lh = p->layers[i];
     // blocked weights [n_out/128][n_in/64][128][64] (pt_tile.cuh tl_to_blocks)
-    if (pt::tc_make_tmap_blocked(&maps[2 * i], Lh.W, Lh.n_in, Lh.n_out, 32, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
-        pt::tc_make_tmap_blocked(&maps[2 * i + 1], Lh.W, Lh.n_in, Lh.n_out, 32, 64,
+    if (pt::tc_make_tmap_blocked(&maps[4 * i], Lh.W, Lh.n_in, Lh.n_out, 32, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        pt::tc_make_tmap_blocked(&maps[4 * i + 1], Lh.W, Lh.n_in, Lh.n_out, 32, 64,
                                  CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
       return fail(PT_ECUDA, "cuTensorMapEncodeTiled failed for layer " + std::to_string(p->layer_base + i));
-    tl[i].tmf = p->d_tmaps + 2 * i;
-    tl[i].tmb = p->d_tmaps + 2 * i + 1;
+    tl[i].tmf = p->d_tmaps + 4 * i;
+    tl[i].tmb = p->d_tmaps + 4 * i + 1;
+    tl[i].tmm = tl[i].tmv = nullptr;
+    if (Lh.mW) {
+      // row-major moments [n_out][ld]: box [64 rows][128 columns] = one backward chunk's update
+      if (pt::tc_make_tmap_2d(&maps[4 * i + 2], Lh.mW, Lh.n_in, Lh.n_out, 128, 64, CU_TENSOR_MAP_SWIZZLE_NONE, Lh.ld_in) ||
+          pt::tc_make_tmap_2d(&maps[4 * i + 3], Lh.vW, Lh.n_in, Lh.n_out, 128, 64, CU_TENSOR_MAP_SWIZZLE_NONE, Lh.ld_in))
+        return fail(PT_ECUDA, "cuTensorMapEncodeTiled failed for the moments of layer " + std::to_string(p->layer_base + i));
+      tl[i].tmm = p->d_tmaps + 4 * i + 2;
+      tl[i].tmv = p->d_tmaps + 4 * i + 3;
+    }
     tl[i].b = Lh.b;
     tl[i].mW = Lh.mW;
     tl[i].vW = Lh.vW;

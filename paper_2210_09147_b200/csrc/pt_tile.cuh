@@ -44,11 +44,22 @@ constexpr int T_TMEM_COLS = 512;
 // the same F/B MMAs with a larger N): ring slots, operand / lo-tile buffers in flight (NB),
 // update-product buffers (NUB), and the TMEM plan = two unit accumulators of 2 TM columns,
 // NB 64-column lo tiles, NUB 128-column update products.
+// build-time overrides of the per-size plan, digits (ring slots, NB, NUB) (tools/variants experiments)
+#ifndef PT_T16_PLAN
+#define PT_T16_PLAN 432
+#endif
+#ifndef PT_T32_PLAN
+#define PT_T32_PLAN 322
+#endif
+#ifndef PT_T64_PLAN
+#define PT_T64_PLAN 211
+#endif
 template <int TM>
 struct TCfg {
-  static constexpr int NSLOT = TM == 16 ? 5 : TM == 32 ? 4 : 3;  // weight ring slots of 32 KB
-  static constexpr int NB = TM == 16 ? 3 : TM == 32 ? 2 : 1;     // chunks in flight between SIMT and MMA
-  static constexpr int NUB = TM == 64 ? 1 : 2;
+  static constexpr int plan = TM == 16 ? PT_T16_PLAN : TM == 32 ? PT_T32_PLAN : PT_T64_PLAN;
+  static constexpr int NSLOT = plan / 100;     // weight ring slots of 32 KB
+  static constexpr int NB = plan / 10 % 10;    // chunks in flight between SIMT and MMA
+  static constexpr int NUB = plan % 10;        // update-product buffers
   static constexpr int ACC_COLS = 2 * T_NACC * 2 * TM;
   static constexpr int LO_COL = ACC_COLS;
   static constexpr int UPD_COL = ACC_COLS + NB * T_CK;
@@ -69,6 +80,7 @@ constexpr int T_DTS = 24;              // dT row stride (floats): conflict-free 
 struct TLayer {
   const CUtensorMap* tmf;  // box [128 rows][32 cols], SWIZZLE_128B
   const CUtensorMap* tmb;  // box [64 rows][32 cols], SWIZZLE_128B_ATOM_32B
+  const CUtensorMap *tmm, *tmv;  // Adam: row-major m, v, box [64 rows][128 cols] (L2 prefetch); else null
   float* b;
   float *mW, *vW, *mb, *vb;  // Adam moments (row-major like W, row pitch ld); null for SGD
   int ld;
@@ -273,6 +285,10 @@ __device__ void t_producer(const TParams& P, const TSmem& sm) {
     for (int i = P.stages[s].first; i < P.stages[s].first + P.stages[s].k; ++i) {
       tma_fence_desc_acquire(P.layers[i].tmf);
       tma_fence_desc_acquire(P.layers[i].tmb);
+      if (P.layers[i].tmm) {
+        tma_fence_desc_acquire(P.layers[i].tmm);
+        tma_fence_desc_acquire(P.layers[i].tmv);
+      }
     }
   // per slot: kind of the chunk it holds (1 forward: released by the MMA commit on sfree,
   // 2 backward: released by the 4 write-back warps on bfree), completions consumed, and a
@@ -350,6 +366,12 @@ __device__ void t_producer(const TParams& P, const TSmem& sm) {
                 tma_load_4d(dst + b * 2048, L.tmb, cc & 63, r0 & 127, cc >> 6, r0 >> 7, &sm.full[slot]);
               }
               if (upd) {
+                if (L.tmm) {
+                  // Adam: pull this chunk's moments into L2 now, a ring's depth before the
+                  // write-back group's update reads them
+                  tma_prefetch_2d(L.tmm, c0, r0);
+                  tma_prefetch_2d(L.tmv, c0, r0);
+                }
                 pend[slot] = true;
                 pend_l[slot] = sp.L;
                 pend_r[slot] = r0;
