@@ -144,7 +144,7 @@ int64_t pt_tick(pt_pipeline* p);
 /* Which device path the handle runs (no reference counterpart; the engine picks it at
  * pt_create): PT_PATH_PANEL = batch-1 panel kernel (16 x 16-tiled weights, column-owned
  * backward; SGD or Adam; PT_PANEL=0 disables), PT_PATH_TILE = tcgen05 tensor-core tile kernel
- * (batch 16, widths % 256 == 0; SGD or Adam, MSE or softmax-CE; PT_TILE=0 disables),
+ * (batch 16, 32 or 64, widths % 256 == 0; SGD or Adam, MSE or softmax-CE; PT_TILE=0 disables),
  * PT_PATH_TICK = row-owned SIMT tick kernel (every other batch and shape). All three run one
  * stage per process / GPU or several stages in one process. Negative = error. */
 #define PT_PATH_TICK 0

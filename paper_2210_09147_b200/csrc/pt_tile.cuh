@@ -573,6 +573,9 @@ __device__ __forceinline__ float t_adam1(float w, float g, float& m, float& v, c
   return w - P.lr * adam_quot(m * c1, v * c2, P.eps);
 }
 
+#ifndef PT_ADAM_RB
+#define PT_ADAM_RB 16  // Adam: moment rows loaded per batch (register budget)
+#endif
 template <bool ADAM>
 __device__ __forceinline__ void t_apply_update(float* tile, uint32_t upd_tmem, float nlr, const TParams& P,
                                                float* mrow, float* vrow, int ld, float c1, float c2) {
@@ -598,15 +601,15 @@ __device__ __forceinline__ void t_apply_update(float* tile, uint32_t upd_tmem, f
 #pragma unroll
       for (int rr = 0; rr < T_UPR; ++rr) g[rr] = d0[rr] + d1[rr];
 #pragma unroll
-      for (int r0 = 0; r0 < T_UPR; r0 += 16) {
-        float mm[16], vv[16];
+      for (int r0 = 0; r0 < T_UPR; r0 += PT_ADAM_RB) {
+        float mm[PT_ADAM_RB], vv[PT_ADAM_RB];
 #pragma unroll
-        for (int q = 0; q < 16; ++q) {
+        for (int q = 0; q < PT_ADAM_RB; ++q) {
           mm[q] = __ldcg(mrow + size_t(rh * T_UPR + r0 + q) * ld + cl);
           vv[q] = __ldcg(vrow + size_t(rh * T_UPR + r0 + q) * ld + cl);
         }
 #pragma unroll
-        for (int q = 0; q < 16; ++q) {
+        for (int q = 0; q < PT_ADAM_RB; ++q) {
           const int rr = r0 + q;
           colp[rr & 3][(rh * T_UPR + rr - (rr & 3)) * 32] = t_adam1(w[rr], g[rr], mm[q], vv[q], P, c1, c2);
           __stcg(mrow + size_t(rh * T_UPR + rr) * ld + cl, mm[q]);

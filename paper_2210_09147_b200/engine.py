@@ -431,7 +431,7 @@ class Pipeline:
 
     @property
     def kernel_path(self):
-        """'panel' (batch-1 panel kernel, SGD or Adam), 'tile' (tcgen05 tensor-core tile kernel, batch 16)
+        """'panel' (batch-1 panel kernel, SGD or Adam), 'tile' (tcgen05 tensor-core tile kernel, micro-batch 16/32/64)
         or 'tick' (row-owned SIMT tick kernel, every other case)."""
         r = self._lib.pt_kernel_path(self._h)
         if r < 0:
