@@ -573,12 +573,42 @@ __device__ __forceinline__ float t_adam1(float w, float g, float& m, float& v, c
   return w - P.lr * adam_quot(m * c1, v * c2, P.eps);
 }
 
-#ifndef PT_ADAM_RB
-#define PT_ADAM_RB 16  // Adam: moment rows loaded per batch (register budget)
-#endif
+// Adam step of a B chunk: 16-row quarters, so the update products, weights
+// and moments of one quarter (80 values) stay in registers; the moments of (row, column cl)
+// are coalesced across the warp's columns and issued before the TMEM loads.
+__device__ __forceinline__ void t_apply_adam(float* tile, uint32_t upd_tmem, const TParams& P, float* mrow,
+                                             float* vrow, int ld, float c1, float c2) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int cl = 32 * (warp & 3) + lane;
+  const uint32_t ta = upd_tmem + ((uint32_t(32 * (warp & 3))) << 16);
+#pragma unroll 1
+  for (int rq = 0; rq < T_CK / 16; ++rq) {
+    float mm[16], vv[16], d0[16], d1[16], w[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      mm[q] = __ldcg(mrow + size_t(16 * rq + q) * ld + cl);
+      vv[q] = __ldcg(vrow + size_t(16 * rq + q) * ld + cl);
+    }
+    tmem_ld_32x32b_x16(ta + uint32_t(16 * rq), d0);         // hi*hi + lo*hi
+    tmem_ld_32x32b_x16(ta + uint32_t(T_CK + 16 * rq), d1);  // hi*lo
+#pragma unroll
+    for (int q = 0; q < 16; ++q) w[q] = tile[t_bofs(cl, 16 * rq + q)];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      tile[t_bofs(cl, 16 * rq + q)] = t_adam1(w[q], d0[q] + d1[q], mm[q], vv[q], P, c1, c2);
+      __stcg(mrow + size_t(16 * rq + q) * ld + cl, mm[q]);
+      __stcg(vrow + size_t(16 * rq + q) * ld + cl, vv[q]);
+    }
+  }
+}
+
 template <bool ADAM>
 __device__ __forceinline__ void t_apply_update(float* tile, uint32_t upd_tmem, float nlr, const TParams& P,
                                                float* mrow, float* vrow, int ld, float c1, float c2) {
+  if (ADAM) {
+    t_apply_adam(tile, upd_tmem, P, mrow, vrow, ld, c1, c2);
+    return;
+  }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cl = 32 * (warp & 3) + lane;
   float* colp[4];
@@ -594,33 +624,9 @@ __device__ __forceinline__ void t_apply_update(float* tile, uint32_t upd_tmem, f
     float w[T_UPR];
 #pragma unroll
     for (int rr = 0; rr < T_UPR; ++rr) w[rr] = colp[rr & 3][(rh * T_UPR + rr - (rr & 3)) * 32];
-    if (ADAM) {
-      // Adam: the moments of (row 32 rh + rr, column cl), coalesced across the warp's columns;
-      // 16 rows in flight at a time (register budget)
-      float g[T_UPR];
 #pragma unroll
-      for (int rr = 0; rr < T_UPR; ++rr) g[rr] = d0[rr] + d1[rr];
-#pragma unroll
-      for (int r0 = 0; r0 < T_UPR; r0 += PT_ADAM_RB) {
-        float mm[PT_ADAM_RB], vv[PT_ADAM_RB];
-#pragma unroll
-        for (int q = 0; q < PT_ADAM_RB; ++q) {
-          mm[q] = __ldcg(mrow + size_t(rh * T_UPR + r0 + q) * ld + cl);
-          vv[q] = __ldcg(vrow + size_t(rh * T_UPR + r0 + q) * ld + cl);
-        }
-#pragma unroll
-        for (int q = 0; q < PT_ADAM_RB; ++q) {
-          const int rr = r0 + q;
-          colp[rr & 3][(rh * T_UPR + rr - (rr & 3)) * 32] = t_adam1(w[rr], g[rr], mm[q], vv[q], P, c1, c2);
-          __stcg(mrow + size_t(rh * T_UPR + rr) * ld + cl, mm[q]);
-          __stcg(vrow + size_t(rh * T_UPR + rr) * ld + cl, vv[q]);
-        }
-      }
-    } else {
-#pragma unroll
-      for (int rr = 0; rr < T_UPR; ++rr)
-        colp[rr & 3][(rh * T_UPR + rr - (rr & 3)) * 32] = fmaf(nlr, d0[rr] + d1[rr], w[rr]);
-    }
+    for (int rr = 0; rr < T_UPR; ++rr)
+      colp[rr & 3][(rh * T_UPR + rr - (rr & 3)) * 32] = fmaf(nlr, d0[rr] + d1[rr], w[rr]);
   }
 }
 
