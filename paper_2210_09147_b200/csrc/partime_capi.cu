@@ -594,28 +594,18 @@ int setup_tile(pt_pipeline* p) {
   PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&p->t_delta), size_t(M) * maxn * 4));
   PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&p->t_bars), 32 * sizeof(u64)));
   PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&p->t_ce), size_t(p->G) * M * 2 * 4));
-  // per layer: W forward / backward boxes, and with Adam the L2-prefetch maps of m and v
-  std::vector<CUtensorMap> maps(4 * p->layers.size());
+  std::vector<CUtensorMap> maps(2 * p->layers.size());
   std::vector<pt::TLayer> tl(p->layers.size());
   PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&p->d_tmaps), maps.size() * sizeof(CUtensorMap)));
   for (size_t i = 0; i < p->layers.size(); ++i) {
     const LayerHost& Lh = p->layers[i];
     // blocked weights [n_out/128][n_in/64][128][64] (pt_tile.cuh tl_to_blocks)
-    if (pt::tc_make_tmap_blocked(&maps[4 * i], Lh.W, Lh.n_in, Lh.n_out, 32, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
-        pt::tc_make_tmap_blocked(&maps[4 * i + 1], Lh.W, Lh.n_in, Lh.n_out, 32, 64,
+    if (pt::tc_make_tmap_blocked(&maps[2 * i], Lh.W, Lh.n_in, Lh.n_out, 32, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
+        pt::tc_make_tmap_blocked(&maps[2 * i + 1], Lh.W, Lh.n_in, Lh.n_out, 32, 64,
                                  CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
       return fail(PT_ECUDA, "cuTensorMapEncodeTiled failed for layer " + std::to_string(p->layer_base + i));
-    tl[i].tmf = p->d_tmaps + 4 * i;
-    tl[i].tmb = p->d_tmaps + 4 * i + 1;
-    tl[i].tmm = tl[i].tmv = nullptr;
-    if (Lh.mW) {
-      // row-major moments [n_out][ld]: box [64 rows][128 columns] = one backward chunk's update
-      if (pt::tc_make_tmap_2d(&maps[4 * i + 2], Lh.mW, Lh.n_in, Lh.n_out, 128, 64, CU_TENSOR_MAP_SWIZZLE_NONE, Lh.ld_in) ||
-          pt::tc_make_tmap_2d(&maps[4 * i + 3], Lh.vW, Lh.n_in, Lh.n_out, 128, 64, CU_TENSOR_MAP_SWIZZLE_NONE, Lh.ld_in))
-        return fail(PT_ECUDA, "cuTensorMapEncodeTiled failed for the moments of layer " + std::to_string(p->layer_base + i));
-      tl[i].tmm = p->d_tmaps + 4 * i + 2;
-      tl[i].tmv = p->d_tmaps + 4 * i + 3;
-    }
+    tl[i].tmf = p->d_tmaps + 2 * i;
+    tl[i].tmb = p->d_tmaps + 2 * i + 1;
     tl[i].b = Lh.b;
     tl[i].mW = Lh.mW;
     tl[i].vW = Lh.vW;
@@ -962,7 +952,8 @@ int create_impl(const pt_config* c, pt_pipeline* p) {
     }
     PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&Lh.b), size_t(Lh.n_out) * 4));
     if (p->opt == PT_OPT_ADAM && p->learn) {
-      // moments in the weights' layout: row-major [n_out][ld_in], or the panel path's tiles
+      // moments: row-major [n_out][ld_in] (tick kernel), the panel path's tiles, or the tile
+      // path's blocked [n_out/128][n_in/64][128][64] (within the same allocation size)
       const size_t nm = p->panel ? size_t(Lh.R) * Lh.C * pt::PN_TILE : size_t(Lh.n_out) * Lh.ld_in;
       PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&Lh.mW), nm * 4));
       PT_TRY(dev_alloc(p, reinterpret_cast<void**>(&Lh.vW), nm * 4));

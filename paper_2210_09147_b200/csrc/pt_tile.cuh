@@ -80,9 +80,8 @@ constexpr int T_DTS = 24;              // dT row stride (floats): conflict-free 
 struct TLayer {
   const CUtensorMap* tmf;  // box [128 rows][32 cols], SWIZZLE_128B
   const CUtensorMap* tmb;  // box [64 rows][32 cols], SWIZZLE_128B_ATOM_32B
-  const CUtensorMap *tmm, *tmv;  // Adam: row-major m, v, box [64 rows][128 cols] (L2 prefetch); else null
   float* b;
-  float *mW, *vW, *mb, *vb;  // Adam moments (row-major like W, row pitch ld); null for SGD
+  float *mW, *vW, *mb, *vb;  // Adam moments (m, v blocked like W: [n_out/128][n_in/64][128][64]); null for SGD
   int ld;
   int n_in, n_out, act;
   int a_in, a_out;  // offsets (floats) of a_i, a_{i+1} in a stage cache slot ([M][n] each)
@@ -285,10 +284,6 @@ __device__ void t_producer(const TParams& P, const TSmem& sm) {
     for (int i = P.stages[s].first; i < P.stages[s].first + P.stages[s].k; ++i) {
       tma_fence_desc_acquire(P.layers[i].tmf);
       tma_fence_desc_acquire(P.layers[i].tmb);
-      if (P.layers[i].tmm) {
-        tma_fence_desc_acquire(P.layers[i].tmm);
-        tma_fence_desc_acquire(P.layers[i].tmv);
-      }
     }
   // per slot: kind of the chunk it holds (1 forward: released by the MMA commit on sfree,
   // 2 backward: released by the 4 write-back warps on bfree), completions consumed, and a
@@ -366,11 +361,15 @@ __device__ void t_producer(const TParams& P, const TSmem& sm) {
                 tma_load_4d(dst + b * 2048, L.tmb, cc & 63, r0 & 127, cc >> 6, r0 >> 7, &sm.full[slot]);
               }
               if (upd) {
-                if (L.tmm) {
+                if (L.mW) {
                   // Adam: pull this chunk's moments into L2 now, a ring's depth before the
-                  // write-back group's update reads them
-                  tma_prefetch_2d(L.tmm, c0, r0);
-                  tma_prefetch_2d(L.tmv, c0, r0);
+                  // write-back group's update reads them (rows r0.. of two 128 x 64 blocks:
+                  // 16 KB contiguous each)
+                  const size_t o = (size_t(r0 >> 7) * (L.n_in >> 6) + (c0 >> 6)) * 8192 + size_t(r0 & 127) * 64;
+                  prefetch_l2(L.mW + o, 16384);
+                  prefetch_l2(L.mW + o + 8192, 16384);
+                  prefetch_l2(L.vW + o, 16384);
+                  prefetch_l2(L.vW + o + 8192, 16384);
                 }
                 pend[slot] = true;
                 pend_l[slot] = sp.L;
@@ -574,20 +573,58 @@ __device__ __forceinline__ float t_adam1(float w, float g, float& m, float& v, c
 }
 
 // Adam step of a B chunk: 16-row quarters, so the update products, weights
-// and moments of one quarter (80 values) stay in registers; the moments of (row, column cl)
-// are coalesced across the warp's columns and issued before the TMEM loads.
+// and moments of one quarter (80 values) stay in registers. mrow / vrow: the chunk's first
+// row of the unit's column block, in the blocked moment layout; thread cl reads its column,
+// so a warp's loads are 128 B contiguous and a chunk's moments are two 16 KB runs each.
 __device__ __forceinline__ void t_apply_adam(float* tile, uint32_t upd_tmem, const TParams& P, float* mrow,
-                                             float* vrow, int ld, float c1, float c2) {
+                                             float* vrow, int, float c1, float c2) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cl = 32 * (warp & 3) + lane;
+  mrow += (cl >> 6) * 8192 + (cl & 63);  // column block blk * 2 + cl / 64 of the unit
+  vrow += (cl >> 6) * 8192 + (cl & 63);
+  constexpr int ld = 64;
   const uint32_t ta = upd_tmem + ((uint32_t(32 * (warp & 3))) << 16);
+#ifdef PT_ADAM_PIPE
+  // the next quarter's moments are in flight while this quarter is updated
+  float mm[16], vv[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    mm[q] = __ldcg(mrow + size_t(q) * ld);
+    vv[q] = __ldcg(vrow + size_t(q) * ld);
+  }
+#pragma unroll 1
+  for (int rq = 0; rq < T_CK / 16; ++rq) {
+    float mn[16], vn[16], d0[16], d1[16], w[16];
+    const int rn = rq + 1 < T_CK / 16 ? 16 * (rq + 1) : 16 * rq;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      mn[q] = __ldcg(mrow + size_t(rn + q) * ld);
+      vn[q] = __ldcg(vrow + size_t(rn + q) * ld);
+    }
+    tmem_ld_32x32b_x16(ta + uint32_t(16 * rq), d0);
+    tmem_ld_32x32b_x16(ta + uint32_t(T_CK + 16 * rq), d1);
+#pragma unroll
+    for (int q = 0; q < 16; ++q) w[q] = tile[t_bofs(cl, 16 * rq + q)];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      tile[t_bofs(cl, 16 * rq + q)] = t_adam1(w[q], d0[q] + d1[q], mm[q], vv[q], P, c1, c2);
+      __stcg(mrow + size_t(16 * rq + q) * ld, mm[q]);
+      __stcg(vrow + size_t(16 * rq + q) * ld, vv[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      mm[q] = mn[q];
+      vv[q] = vn[q];
+    }
+  }
+#else
 #pragma unroll 1
   for (int rq = 0; rq < T_CK / 16; ++rq) {
     float mm[16], vv[16], d0[16], d1[16], w[16];
 #pragma unroll
     for (int q = 0; q < 16; ++q) {
-      mm[q] = __ldcg(mrow + size_t(16 * rq + q) * ld + cl);
-      vv[q] = __ldcg(vrow + size_t(16 * rq + q) * ld + cl);
+      mm[q] = __ldcg(mrow + size_t(16 * rq + q) * ld);
+      vv[q] = __ldcg(vrow + size_t(16 * rq + q) * ld);
     }
     tmem_ld_32x32b_x16(ta + uint32_t(16 * rq), d0);         // hi*hi + lo*hi
     tmem_ld_32x32b_x16(ta + uint32_t(T_CK + 16 * rq), d1);  // hi*lo
@@ -596,10 +633,11 @@ __device__ __forceinline__ void t_apply_adam(float* tile, uint32_t upd_tmem, con
 #pragma unroll
     for (int q = 0; q < 16; ++q) {
       tile[t_bofs(cl, 16 * rq + q)] = t_adam1(w[q], d0[q] + d1[q], mm[q], vv[q], P, c1, c2);
-      __stcg(mrow + size_t(16 * rq + q) * ld + cl, mm[q]);
-      __stcg(vrow + size_t(16 * rq + q) * ld + cl, vv[q]);
+      __stcg(mrow + size_t(16 * rq + q) * ld, mm[q]);
+      __stcg(vrow + size_t(16 * rq + q) * ld, vv[q]);
     }
   }
+#endif
 }
 
 template <bool ADAM>
@@ -921,7 +959,8 @@ __global__ void __launch_bounds__(T_THREADS, 1) tile_kernel(const __grid_constan
                 t_trace(P, tr, 9);
                 if (upd) {
                   // Adam: this chunk's rows r0.. and the unit's 128 columns c0.. of the moments
-                  const size_t mo = size_t(q * (L.n_out / T_Q) + chn * T_CK) * L.ld + size_t(blk) * 128;
+                  const int mr0 = q * (L.n_out / T_Q) + chn * T_CK;  // blocked moments (see TLayer)
+                  const size_t mo = (size_t(mr0 >> 7) * (L.n_in >> 6) + size_t(blk) * 2) * 8192 + size_t(mr0 & 127) * 64;
                   t_apply_update<OPT == 1>(sm.ring + size_t(pslot) * T_SLOT_FLOATS, tbase + C::UPD_COL + (bb % C::NUB) * 128, nlr, P,
                                  OPT == 1 ? L.mW + mo : nullptr, OPT == 1 ? L.vW + mo : nullptr, L.ld, c1, c2);
                   fence_proxy_async_shared();  // W' -> the producer's TMA store
