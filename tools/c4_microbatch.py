@@ -5,8 +5,9 @@ sys.path.insert(0, '.')
 import bench
 from paper_2210_09147_b200 import engine, model as mdl, streams
 Ms = [int(a) for a in sys.argv[1].split(",")] if len(sys.argv) > 1 else [16, 32, 64]
+OPTS = sys.argv[2].split(",") if len(sys.argv) > 2 else ["sgd", "adam"]
 for M in Ms:
-    for opt in ("sgd", "adam"):
+    for opt in OPTS:
         w = [4096]*33
         m = mdl.mlp(w, seed=0, dtype=np.float32)
         st = streams.SmoothStream(4096, 4096, seed=1, batch=M)

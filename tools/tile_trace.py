@@ -9,12 +9,12 @@ NAMES = {1: "compute.begin", 2: "compute.end", 3: "barrier1", 4: "finalize", 5: 
          7: "full.seen", 11: "mdone.j-2", 12: "opnd.rdy", 13: "lopass.end", 22: "mma.hi.issued", 23: "mma.prep.seen", 8: "prep.done", 8: "grpB.wait", 9: "grpB.mdone", 10: "grpB.done", 14: "update.math", 20: "mma.prep", 21: "mma.commit",
          30: "tma.issue"}
 
-def run(widths, counts, ticks=2, M=16, learn=True, cta=0):
+def run(widths, counts, ticks=2, M=16, learn=True, cta=0, opt="sgd"):
     m = mdl.mlp(widths, seed=0)
     st = streams.SmoothStream(widths[0], widths[-1], seed=1, batch=M)
     xs, ys = st.block(0, ticks)
     xs = torch.tensor(xs, dtype=torch.float32, device="cuda"); ys = torch.tensor(ys, dtype=torch.float32, device="cuda")
-    p = engine.Pipeline(m, counts, "sgd", 1e-3 if learn else 0.0, xs[0].cpu().numpy(), ys[0].cpu().numpy(), learn=learn)
+    p = engine.Pipeline(m, counts, opt, (1e-3 if opt == "sgd" else 1e-4) if learn else 0.0, xs[0].cpu().numpy(), ys[0].cpu().numpy(), learn=learn)
     assert p.kernel_path == "tile", p.kernel_path
     p.run(xs, ys); p.sync()
     p.set_trace(cta, 1 << 14)
@@ -36,7 +36,7 @@ def run(widths, counts, ticks=2, M=16, learn=True, cta=0):
             v = np.array(d[k])
             print(f"  group B {NAMES.get(k[0], k[0]):>12} -> {NAMES.get(k[1], k[1]):<12} n={len(v):4d} median={np.median(v) / 1e3:6.2f}us total={v.sum() / 1e3 / ticks:8.1f}us/tick")
     L = len(widths) - 1
-    print(f"== {widths[0]}x{L} M={M} learn={learn} counts={counts}: {ms * 1e3 / ticks:.1f} us/tick")
+    print(f"== {widths[0]}x{L} M={M} {opt} learn={learn} counts={counts}: {ms * 1e3 / ticks:.1f} us/tick")
     dur = defaultdict(list)
     for (c0, t0), (c1, t1) in zip(cons, cons[1:]):
         dur[(c0, c1)].append(t1 - t0)
@@ -71,5 +71,8 @@ def run(widths, counts, ticks=2, M=16, learn=True, cta=0):
     p.close()
 
 if __name__ == "__main__":
-    run([4096] * 9, [15], ticks=2, learn=False)
-    run([4096] * 9, [15], ticks=2)
+    if len(sys.argv) > 1:  # optimizer (sgd / adam), micro-batch
+        run([4096] * 9, [15], ticks=2, opt=sys.argv[1], M=int(sys.argv[2]) if len(sys.argv) > 2 else 16)
+    else:
+        run([4096] * 9, [15], ticks=2, learn=False)
+        run([4096] * 9, [15], ticks=2)
