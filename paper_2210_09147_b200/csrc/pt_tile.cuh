@@ -584,40 +584,6 @@ __device__ __forceinline__ void t_apply_adam(float* tile, uint32_t upd_tmem, con
   vrow += (cl >> 6) * 8192 + (cl & 63);
   constexpr int ld = 64;
   const uint32_t ta = upd_tmem + ((uint32_t(32 * (warp & 3))) << 16);
-#ifdef PT_ADAM_PIPE
-  // the next quarter's moments are in flight while this quarter is updated
-  float mm[16], vv[16];
-#pragma unroll
-  for (int q = 0; q < 16; ++q) {
-    mm[q] = __ldcg(mrow + size_t(q) * ld);
-    vv[q] = __ldcg(vrow + size_t(q) * ld);
-  }
-#pragma unroll 1
-  for (int rq = 0; rq < T_CK / 16; ++rq) {
-    float mn[16], vn[16], d0[16], d1[16], w[16];
-    const int rn = rq + 1 < T_CK / 16 ? 16 * (rq + 1) : 16 * rq;
-#pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      mn[q] = __ldcg(mrow + size_t(rn + q) * ld);
-      vn[q] = __ldcg(vrow + size_t(rn + q) * ld);
-    }
-    tmem_ld_32x32b_x16(ta + uint32_t(16 * rq), d0);
-    tmem_ld_32x32b_x16(ta + uint32_t(T_CK + 16 * rq), d1);
-#pragma unroll
-    for (int q = 0; q < 16; ++q) w[q] = tile[t_bofs(cl, 16 * rq + q)];
-#pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      tile[t_bofs(cl, 16 * rq + q)] = t_adam1(w[q], d0[q] + d1[q], mm[q], vv[q], P, c1, c2);
-      __stcg(mrow + size_t(16 * rq + q) * ld, mm[q]);
-      __stcg(vrow + size_t(16 * rq + q) * ld, vv[q]);
-    }
-#pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      mm[q] = mn[q];
-      vv[q] = vn[q];
-    }
-  }
-#else
 #pragma unroll 1
   for (int rq = 0; rq < T_CK / 16; ++rq) {
     float mm[16], vv[16], d0[16], d1[16], w[16];
@@ -637,7 +603,6 @@ __device__ __forceinline__ void t_apply_adam(float* tile, uint32_t upd_tmem, con
       __stcg(vrow + size_t(16 * rq + q) * ld, vv[q]);
     }
   }
-#endif
 }
 
 template <bool ADAM>
