@@ -645,7 +645,10 @@ int setup_tile(pt_pipeline* p) {
   p->t_layers_host = tl;
   PT_TRY(upload_tile_stages(p));
   // shared memory: 1 KB alignment slack, ring, operands, update operands, reductions, barriers
-  p->t_smem = M == 16 ? pt::TCfg<16>::smem_bytes() : M == 32 ? pt::TCfg<32>::smem_bytes() : pt::TCfg<64>::smem_bytes();
+  if (p->opt == PT_OPT_ADAM)
+    p->t_smem = M == 16 ? pt::TCfg<16, 1>::smem_bytes() : M == 32 ? pt::TCfg<32, 1>::smem_bytes() : pt::TCfg<64, 1>::smem_bytes();
+  else
+    p->t_smem = M == 16 ? pt::TCfg<16>::smem_bytes() : M == 32 ? pt::TCfg<32>::smem_bytes() : pt::TCfg<64>::smem_bytes();
   if (p->t_smem > pt::SMEM_MAX) return fail(PT_EINVAL, "tile path shared-memory plan exceeds 227 KB");
   CUDA_TRY(cudaFuncSetAttribute(tile_fn(p), cudaFuncAttributeMaxDynamicSharedMemorySize, p->t_smem));
   return PT_OK;

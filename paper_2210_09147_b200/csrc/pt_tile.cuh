@@ -44,7 +44,8 @@ constexpr int T_TMEM_COLS = 512;
 // the same F/B MMAs with a larger N): ring slots, operand / lo-tile buffers in flight (NB),
 // update-product buffers (NUB), and the TMEM plan = two unit accumulators of 2 TM columns,
 // NB 64-column lo tiles, NUB 128-column update products.
-// build-time overrides of the per-size plan, digits (ring slots, NB, NUB) (tools/variants experiments)
+// build-time overrides of the per-size plan, digits (ring slots, NB, NUB) (tools/variants experiments);
+// Adam (OPT = 1) holds a ring slot longer per backward chunk and runs best one slot shallower
 #ifndef PT_T16_PLAN
 #define PT_T16_PLAN 432
 #endif
@@ -54,9 +55,19 @@ constexpr int T_TMEM_COLS = 512;
 #ifndef PT_T64_PLAN
 #define PT_T64_PLAN 211
 #endif
-template <int TM>
+#ifndef PT_T16_PLAN_ADAM
+#define PT_T16_PLAN_ADAM 332
+#endif
+#ifndef PT_T32_PLAN_ADAM
+#define PT_T32_PLAN_ADAM 222
+#endif
+#ifndef PT_T64_PLAN_ADAM
+#define PT_T64_PLAN_ADAM 211
+#endif
+template <int TM, int OPT = 0>
 struct TCfg {
-  static constexpr int plan = TM == 16 ? PT_T16_PLAN : TM == 32 ? PT_T32_PLAN : PT_T64_PLAN;
+  static constexpr int plan = OPT == 1 ? (TM == 16 ? PT_T16_PLAN_ADAM : TM == 32 ? PT_T32_PLAN_ADAM : PT_T64_PLAN_ADAM)
+                                       : (TM == 16 ? PT_T16_PLAN : TM == 32 ? PT_T32_PLAN : PT_T64_PLAN);
   static constexpr int NSLOT = plan / 100;     // weight ring slots of 32 KB
   static constexpr int NB = plan / 10 % 10;    // chunks in flight between SIMT and MMA
   static constexpr int NUB = plan % 10;        // update-product buffers
@@ -70,11 +81,14 @@ struct TCfg {
            TM * 4 + (3 * NSLOT + 5 * NB + 4) * 8 + 16;
   }
 };
-template <int TM>
+template <int TM, int OPT>
 constexpr bool tcfg_fits() {
-  return TCfg<TM>::UPD_COL + TCfg<TM>::NUB * 128 <= T_TMEM_COLS && TCfg<TM>::smem_bytes() <= 227 * 1024;
+  using C = TCfg<TM, OPT>;
+  return C::UPD_COL + C::NUB * 128 <= T_TMEM_COLS && C::smem_bytes() <= 227 * 1024;
 }
-static_assert(tcfg_fits<16>() && tcfg_fits<32>() && tcfg_fits<64>(), "tile kernel TMEM / shared-memory plan");
+static_assert(tcfg_fits<16, 0>() && tcfg_fits<32, 0>() && tcfg_fits<64, 0>() && tcfg_fits<16, 1>() &&
+                  tcfg_fits<32, 1>() && tcfg_fits<64, 1>(),
+              "tile kernel TMEM / shared-memory plan");
 constexpr int T_DTS = 24;              // dT row stride (floats): conflict-free staging, 16-B rows
 
 struct TLayer {
@@ -275,9 +289,9 @@ struct TSmem {
 };
 
 // ------------------------------------------------------------------ producer
-template <int TM>
+template <int TM, int OPT>
 __device__ void t_producer(const TParams& P, const TSmem& sm) {
-  using C = TCfg<TM>;
+  using C = TCfg<TM, OPT>;
   const int c = blockIdx.x, G = P.G;
   uint32_t j = 0;
   for (int s = 0; s < P.n_stages; ++s)
@@ -394,9 +408,9 @@ __device__ void t_producer(const TParams& P, const TSmem& sm) {
 }
 
 // ------------------------------------------------------------------ MMA issuer
-template <int TM>
+template <int TM, int OPT>
 __device__ void t_mma(const TParams& P, const TSmem& sm, uint32_t tbase) {
-  using C = TCfg<TM>;
+  using C = TCfg<TM, OPT>;
   // Per K-step two MMAs: hi(W) x [a_hi; a_lo] (N = 2M) and lo(W) x a_hi (N = M), both into
   // the unit accumulator: columns [0, M) collect hi*a_hi + lo*a_hi, [M, 2M) hi*a_lo.
   // The hi MMAs read the raw TMA tile (the tensor core uses its top 19 bits = tf32(w)),
@@ -709,7 +723,7 @@ __global__ void tl_from_blocks(const float* __restrict__ src, float* __restrict_
 // SGD kernel)
 template <int OPT, int TM>
 __global__ void __launch_bounds__(T_THREADS, 1) tile_kernel(const __grid_constant__ TParams P) {
-  using C = TCfg<TM>;
+  using C = TCfg<TM, OPT>;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1024-B alignment of the swizzled tiles
   // (pointer arithmetic on smem_raw, not integer casts, so the compiler keeps the shared
@@ -763,9 +777,9 @@ __global__ void __launch_bounds__(T_THREADS, 1) tile_kernel(const __grid_constan
   const uint32_t tbase = *sm.tmem;
 
   if (warp == 0) {
-    if (lane == 0) t_producer<TM>(P, sm);
+    if (lane == 0) t_producer<TM, OPT>(P, sm);
   } else if (warp == 1) {
-    if (lane == 0) t_mma<TM>(P, sm, tbase);
+    if (lane == 0) t_mma<TM, OPT>(P, sm, tbase);
   } else {
     // ================================================================ SIMT
     const int st_id = tid - T_SIMT0;           // 0..255
