@@ -37,7 +37,10 @@ constexpr int T_SIMT0 = 64;            // first SIMT thread
 constexpr int T_NS = 256;              // SIMT threads
 constexpr int T_SLOT_FLOATS = 8192;
 constexpr int T_CK = 64;               // F: chunk columns; B: chunk rows
-constexpr int T_Q = 4;                 // quarters (columns in F, rows in B)
+#ifndef PT_TQ
+#define PT_TQ 4
+#endif
+constexpr int T_Q = PT_TQ;             // quarters (columns in F, rows in B)
 constexpr int T_NACC = 1;              // independent accumulators per unit (K-step % T_NACC)
 constexpr int T_TMEM_COLS = 512;
 // Per micro-batch size TM (16, 32 or 64; the batch is the MMA's N side, so a larger TM issues
